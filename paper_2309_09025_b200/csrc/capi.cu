@@ -1,0 +1,768 @@
+// capi.cu — C ABI of libfdsnn_b200.so (declared in include/fdsnn_b200.h).
+// One translation unit: includes the kernel headers and owns the context,
+// device key storage, scratch buffers, launch dispatch and instrumentation.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fdsnn_b200.h"
+#include "keyswitch.cuh"
+#include "linear.cuh"
+#include "pbs.cuh"
+
+using namespace fdsnn;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_err(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define CU(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return set_err(FDSNN_ERR_CUDA, "%s failed: %s (%s:%d)", #call,              \
+                           cudaGetErrorString(e_), __FILE__, __LINE__);                 \
+    } while (0)
+
+bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+int ilog2(int64_t x) { int r = 0; while ((1ll << r) < x) ++r; return r; }
+int round4(int x) { return (x + 3) & ~3; }
+
+struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    int ensure(size_t want) {
+        if (want <= bytes) return FDSNN_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) return set_err(FDSNN_ERR_CUDA, "cudaMalloc(%zu): %s", want, cudaGetErrorString(e));
+        bytes = want;
+        return FDSNN_OK;
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+};
+
+struct Operator {
+    bool dense = true;
+    int out_cells = 0, in_cells = 0;
+    int32_t* w = nullptr;        // dense (out x in)
+    int32_t* row_ptr = nullptr;  // csr
+    int32_t* col_idx = nullptr;
+    int32_t* val = nullptr;
+};
+
+struct TimedLaunch {
+    int which;
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct fdsnn_ctx {
+    fdsnn_params prm{};
+    DevParams dp{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    double2* tables = nullptr;  // W | twist | untw
+    double2* bsk = nullptr;
+    uint32_t* ksk = nullptr;
+    bool keys_loaded = false;
+    std::vector<int32_t*> luts;
+    std::vector<Operator> ops;
+    Buf ext, rows_a, rows_b, rows_c, host_stage, acc_buf, a2n_buf, l2flush;
+    unsigned long long* margin = nullptr;
+    bool track_margin = false;
+    bool timing = false;
+    std::vector<TimedLaunch> timed;
+    double timed_ms[3] = {0, 0, 0};
+    int64_t timed_n[3] = {0, 0, 0};
+    std::mutex mu;
+};
+
+namespace {
+
+struct TimerScope {
+    fdsnn_ctx* ctx;
+    int which;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr, b = nullptr;
+    TimerScope(fdsnn_ctx* c, int w, cudaStream_t st) : ctx(c), which(w), s(st) {
+        if (ctx->timing) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, s);
+        }
+    }
+    ~TimerScope() {
+        if (ctx->timing) {
+            cudaEventRecord(b, s);
+            ctx->timed.push_back({which, a, b});
+        }
+    }
+};
+
+cudaStream_t pick(fdsnn_ctx* ctx, void* stream) {
+    return stream ? reinterpret_cast<cudaStream_t>(stream) : ctx->stream;
+}
+
+template <int M, int G, bool RAW, bool MARGIN>
+int launch_br_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_t s) {
+    const size_t smem = pbs_smem_bytes<M>(G, 2 * M, ctx->dp.n);
+    auto kern = pbs_blind_rotate_kernel<M, G, RAW, MARGIN>;
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t blocks = (V + G - 1) / G;
+    kern<<<(unsigned)blocks, G * (M / 8), smem, s>>>(a);
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
+template <int M, int G>
+int launch_br_m(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_t s) {
+    if (raw) return ctx->track_margin ? launch_br_t<M, G, true, true>(ctx, a, V, s)
+                                      : launch_br_t<M, G, true, false>(ctx, a, V, s);
+    return ctx->track_margin ? launch_br_t<M, G, false, true>(ctx, a, V, s)
+                             : launch_br_t<M, G, false, false>(ctx, a, V, s);
+}
+
+int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_t s) {
+    if (V <= 0) return FDSNN_OK;
+    TimerScope ts(ctx, 0, s);
+    switch (ctx->dp.M) {
+        case 256: return launch_br_m<256, 4>(ctx, a, V, raw, s);
+        case 512: return launch_br_m<512, 2>(ctx, a, V, raw, s);
+        case 1024: return launch_br_m<1024, 1>(ctx, a, V, raw, s);
+    }
+    return set_err(FDSNN_ERR_PARAMETER, "unsupported ring degree N=%d", ctx->dp.N);
+}
+
+template <int KSL>
+int launch_ks_t(fdsnn_ctx* ctx, const KsArgs& a, cudaStream_t s) {
+    dim3 grid((unsigned)((a.V + KS_ROWS - 1) / KS_ROWS), (unsigned)((ctx->dp.n + KS_COLS - 1) / KS_COLS));
+    ks_mask_kernel<KSL><<<grid, 256, 0, s>>>(a);
+    CU(cudaGetLastError());
+    ks_body_kernel<KSL><<<(unsigned)((a.V + 7) / 8), 256, 0, s>>>(a);
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
+int launch_ks(fdsnn_ctx* ctx, const KsArgs& a, cudaStream_t s) {
+    if (a.V <= 0) return FDSNN_OK;
+    TimerScope ts(ctx, 1, s);
+    switch (ctx->dp.ks_L) {
+        case 2: return launch_ks_t<2>(ctx, a, s);
+        case 3: return launch_ks_t<3>(ctx, a, s);
+        case 4: return launch_ks_t<4>(ctx, a, s);
+        case 5: return launch_ks_t<5>(ctx, a, s);
+        case 6: return launch_ks_t<6>(ctx, a, s);
+        case 8: return launch_ks_t<8>(ctx, a, s);
+    }
+    return set_err(FDSNN_ERR_PARAMETER, "unsupported key-switch levels %d", ctx->dp.ks_L);
+}
+
+unsigned grid1d(int64_t work) {
+    int64_t b = (work + 255) / 256;
+    if (b > 148 * 32) b = 148 * 32;
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}
+
+int check_keys(fdsnn_ctx* ctx) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    if (!ctx->keys_loaded) return set_err(FDSNN_ERR_STATE, "bootstrapping key not loaded");
+    return FDSNN_OK;
+}
+
+int check_lut(fdsnn_ctx* ctx, int32_t id) {
+    if (id < 0 || id >= (int32_t)ctx->luts.size())
+        return set_err(FDSNN_ERR_STATE, "unknown LUT id %d", id);
+    return FDSNN_OK;
+}
+
+uint32_t delta_times(fdsnn_ctx* ctx, int64_t k) {
+    const int64_t q = 1ll << ctx->dp.log2q;
+    const int64_t delta = q / ctx->dp.p;
+    return (uint32_t)(((k % ctx->dp.p) * delta % q + q) % q);
+}
+
+// Shared PBS pipeline on device rows: BR (+extract) then KS.
+int pbs_pipeline(fdsnn_ctx* ctx, int nlut, const int32_t* lut_ids, const int64_t* in_boff,
+                 const int64_t* out_boff, const uint32_t* d_in, const uint32_t* d_in2,
+                 int64_t count, uint32_t* d_out, cudaStream_t s) {
+    int rc;
+    if ((rc = check_keys(ctx))) return rc;
+    if (nlut < 1 || nlut > 4) return set_err(FDSNN_ERR_PARAMETER, "nlut must be in [1,4]");
+    if (count <= 0) return FDSNN_OK;
+    PbsArgs a{};
+    a.prm = ctx->dp;
+    a.in = d_in;
+    a.in2 = d_in2;
+    a.count = count;
+    a.nlut = nlut;
+    for (int u = 0; u < nlut; ++u) {
+        if ((rc = check_lut(ctx, lut_ids[u]))) return rc;
+        a.lut[u] = ctx->luts[lut_ids[u]];
+        a.in_boff[u] = in_boff ? delta_times(ctx, in_boff[u]) : 0u;
+    }
+    a.bsk = ctx->bsk;
+    a.tables = ctx->tables;
+    const int64_t V = count * nlut;
+    if ((rc = ctx->ext.ensure((size_t)V * ctx->dp.ext_stride * 4))) return rc;
+    a.ext_out = (uint32_t*)ctx->ext.p;
+    a.margin = ctx->margin;
+    if ((rc = launch_br(ctx, a, V, false, s))) return rc;
+    KsArgs k{};
+    k.prm = ctx->dp;
+    k.ext = (const uint32_t*)ctx->ext.p;
+    k.V = V;
+    k.ksk = ctx->ksk;
+    k.out = d_out;
+    k.count = count;
+    for (int u = 0; u < nlut; ++u) k.out_boff[u] = out_boff ? delta_times(ctx, out_boff[u]) : 0u;
+    return launch_ks(ctx, k, s);
+}
+
+__global__ void fp64_peak_kernel(double* out, int iters) {
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+    double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+    const double m = 0.999999999, c = 1e-12;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+            a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+        }
+    }
+    const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.678) out[0] = s;  // never true; keeps the chain live
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fdsnn_last_error(void) { return g_last_error.c_str(); }
+
+int32_t fdsnn_row_stride(int32_t n) { return round4(n + 1); }
+
+int fdsnn_ctx_create(const fdsnn_params* prm, int32_t device, fdsnn_ctx** out) {
+    if (!prm || !out) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+    const fdsnn_params& p = *prm;
+    if (!(p.N == 512 || p.N == 1024 || p.N == 2048))
+        return set_err(FDSNN_ERR_PARAMETER, "ring degree N=%d not supported (512, 1024, 2048)", p.N);
+    if (p.log2_q < 2 || p.log2_q > 31) return set_err(FDSNN_ERR_PARAMETER, "q must be 2^k with 2<=k<=31");
+    if (!is_pow2(p.p) || p.p % 2 || p.p > 2 * p.N) return set_err(FDSNN_ERR_PARAMETER, "bad message modulus p=%d", p.p);
+    if (p.n < 1 || p.n > 2048) return set_err(FDSNN_ERR_PARAMETER, "LWE dimension n=%d out of range", p.n);
+    if (p.bg_log < 1 || p.levels < 1 || p.bg_log * p.levels < p.log2_q)
+        return set_err(FDSNN_ERR_PARAMETER, "gadget must cover q (base**levels >= q)");
+    if (p.ks_log < 1 || p.ks_levels < 1 || p.ks_log * p.ks_levels < p.log2_q)
+        return set_err(FDSNN_ERR_PARAMETER, "key-switch gadget must cover q");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return set_err(FDSNN_ERR_CUDA, "no CUDA device available (this library has no CPU fallback)");
+    if (device < 0 || device >= ndev) return set_err(FDSNN_ERR_PARAMETER, "bad device %d", device);
+    cudaDeviceProp dprop;
+    CU(cudaGetDeviceProperties(&dprop, device));
+    if (dprop.major != 10) return set_err(FDSNN_ERR_CUDA, "device %s is sm_%d%d; this build targets sm_100a", dprop.name, dprop.major, dprop.minor);
+    CU(cudaSetDevice(device));
+    fdsnn_ctx* ctx = new fdsnn_ctx();
+    ctx->prm = p;
+    ctx->device = device;
+    DevParams& d = ctx->dp;
+    d.n = p.n;
+    d.N = p.N;
+    d.M = p.N / 2;
+    d.log2q = p.log2_q;
+    d.qmask = (uint32_t)((1ull << p.log2_q) - 1);
+    d.bg_log = p.bg_log;
+    d.L = p.levels;
+    d.ks_log = p.ks_log;
+    d.ks_L = p.ks_levels;
+    d.stride = round4(p.n + 1);
+    d.ext_stride = round4(p.N + 1);
+    d.p = p.p;
+    d.half_slot = p.N / p.p;
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return set_err(FDSNN_ERR_CUDA, "stream creation failed");
+    }
+    // transform tables in long double: W[k] = e^{2 pi i k/M}, twist[j] = e^{i pi j/N},
+    // untw[j] = conj(twist[j]) / M   (ring.py:115-118, bootstrap.py:432-436)
+    const int M = d.M;
+    std::vector<double2> tab(3 * M);
+    const long double PI = 3.141592653589793238462643383279502884L;
+    for (int k = 0; k < M; ++k) {
+        long double ang = 2.0L * PI * k / M;
+        tab[k] = make_double2((double)cosl(ang), (double)sinl(ang));
+        long double tw = PI * k / p.N;
+        tab[M + k] = make_double2((double)cosl(tw), (double)sinl(tw));
+        tab[2 * M + k] = make_double2((double)(cosl(tw) / M), (double)(-sinl(tw) / M));
+    }
+    if (cudaMalloc(&ctx->tables, tab.size() * sizeof(double2)) != cudaSuccess ||
+        cudaMemcpy(ctx->tables, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMalloc(&ctx->margin, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(ctx->margin, 0, sizeof(unsigned long long)) != cudaSuccess) {
+        fdsnn_ctx_destroy(ctx);
+        return set_err(FDSNN_ERR_CUDA, "device allocation failed");
+    }
+    *out = ctx;
+    return FDSNN_OK;
+}
+
+int fdsnn_ctx_destroy(fdsnn_ctx* ctx) {
+    if (!ctx) return FDSNN_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto& t : ctx->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+    for (auto* l : ctx->luts) cudaFree(l);
+    for (auto& o : ctx->ops) { cudaFree(o.w); cudaFree(o.row_ptr); cudaFree(o.col_idx); cudaFree(o.val); }
+    cudaFree(ctx->tables);
+    cudaFree(ctx->bsk);
+    cudaFree(ctx->ksk);
+    cudaFree(ctx->margin);
+    ctx->ext.release(); ctx->rows_a.release(); ctx->rows_b.release(); ctx->rows_c.release();
+    ctx->host_stage.release(); ctx->acc_buf.release(); ctx->a2n_buf.release(); ctx->l2flush.release();
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return FDSNN_OK;
+}
+
+void* fdsnn_ctx_stream(fdsnn_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int fdsnn_bsk_load(fdsnn_ctx* ctx, const int64_t* rows, const int64_t* ksk_A, const int64_t* ksk_b) {
+    if (!ctx || !rows || !ksk_A || !ksk_b) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CU(cudaSetDevice(ctx->device));
+    const DevParams& d = ctx->dp;
+    const int64_t npoly = (int64_t)d.n * 2 * d.L * 2;
+    const size_t row_bytes = (size_t)npoly * d.N * sizeof(int64_t);
+    int64_t* d_rows = nullptr;
+    CU(cudaMalloc(&d_rows, row_bytes));
+    CU(cudaMemcpyAsync(d_rows, rows, row_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    if (!ctx->bsk) CU(cudaMalloc(&ctx->bsk, (size_t)npoly * d.M * sizeof(double2)));
+    {
+        const int M = d.M;
+        const int T = M / 8;
+        const int G = 128 / T > 0 ? 128 / T : 1;
+        const size_t smem = 3 * (size_t)M * sizeof(double2) + (size_t)G * 2 * (M + M / 8) * sizeof(double2);
+        const unsigned blocks = (unsigned)((npoly + G - 1) / G);
+        switch (M) {
+            case 256:
+                CU(cudaFuncSetAttribute(bsk_forward_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                bsk_forward_kernel<256, 4><<<blocks, 128, smem, ctx->stream>>>(d_rows, npoly, d.log2q, ctx->tables, ctx->bsk);
+                break;
+            case 512:
+                CU(cudaFuncSetAttribute(bsk_forward_kernel<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                bsk_forward_kernel<512, 2><<<blocks, 128, smem, ctx->stream>>>(d_rows, npoly, d.log2q, ctx->tables, ctx->bsk);
+                break;
+            case 1024:
+                CU(cudaFuncSetAttribute(bsk_forward_kernel<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                bsk_forward_kernel<1024, 1><<<blocks, 128, smem, ctx->stream>>>(d_rows, npoly, d.log2q, ctx->tables, ctx->bsk);
+                break;
+        }
+        CU(cudaGetLastError());
+    }
+    // KSK: (N*ks_L) x stride uint32 [A | b | 0]
+    const int64_t krows = (int64_t)d.N * d.ks_L;
+    std::vector<uint32_t> kh((size_t)krows * d.stride, 0u);
+    for (int64_t r = 0; r < krows; ++r) {
+        for (int c = 0; c < d.n; ++c) kh[r * d.stride + c] = (uint32_t)ksk_A[r * d.n + c] & d.qmask;
+        kh[r * d.stride + d.n] = (uint32_t)ksk_b[r] & d.qmask;
+    }
+    if (!ctx->ksk) CU(cudaMalloc(&ctx->ksk, kh.size() * 4));
+    CU(cudaMemcpyAsync(ctx->ksk, kh.data(), kh.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaFree(d_rows));
+    ctx->keys_loaded = true;
+    return FDSNN_OK;
+}
+
+int fdsnn_lut_load(fdsnn_ctx* ctx, const int64_t* testpoly, int32_t* lut_id) {
+    if (!ctx || !testpoly || !lut_id) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CU(cudaSetDevice(ctx->device));
+    std::vector<int32_t> h(ctx->dp.N);
+    for (int j = 0; j < ctx->dp.N; ++j) h[j] = (int32_t)((uint32_t)testpoly[j] & ctx->dp.qmask);
+    int32_t* d = nullptr;
+    CU(cudaMalloc(&d, h.size() * 4));
+    CU(cudaMemcpy(d, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    ctx->luts.push_back(d);
+    *lut_id = (int32_t)ctx->luts.size() - 1;
+    return FDSNN_OK;
+}
+
+int fdsnn_rows_from_host(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b, int64_t count,
+                         uint32_t* d_rows, void* stream) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    if (count <= 0) return FDSNN_OK;
+    cudaStream_t s = pick(ctx, stream);
+    const DevParams& d = ctx->dp;
+    const size_t abytes = (size_t)count * d.n * 8, bbytes = (size_t)count * 8;
+    int rc;
+    if ((rc = ctx->host_stage.ensure(abytes + bbytes))) return rc;
+    int64_t* dA = (int64_t*)ctx->host_stage.p;
+    int64_t* db = dA + (size_t)count * d.n;
+    CU(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(db, b, bbytes, cudaMemcpyHostToDevice, s));
+    rows_pack_kernel<<<grid1d(count * d.stride), 256, 0, s>>>(dA, db, count, d.n, d.stride, d.qmask, d_rows);
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
+int fdsnn_rows_to_host(fdsnn_ctx* ctx, const uint32_t* d_rows, int64_t count, int64_t* A,
+                       int64_t* b, void* stream) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    if (count <= 0) return FDSNN_OK;
+    cudaStream_t s = pick(ctx, stream);
+    const DevParams& d = ctx->dp;
+    const size_t abytes = (size_t)count * d.n * 8, bbytes = (size_t)count * 8;
+    int rc;
+    if ((rc = ctx->host_stage.ensure(abytes + bbytes))) return rc;
+    int64_t* dA = (int64_t*)ctx->host_stage.p;
+    int64_t* db = dA + (size_t)count * d.n;
+    rows_unpack_kernel<<<grid1d(count * (d.n + 1)), 256, 0, s>>>(d_rows, count, d.n, d.stride, dA, db);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(A, dA, abytes, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(b, db, bbytes, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    return FDSNN_OK;
+}
+
+int fdsnn_pbs_dev(fdsnn_ctx* ctx, int32_t nlut, const int32_t* lut_ids, const int64_t* in_boff,
+                  const int64_t* out_boff, const uint32_t* d_in, const uint32_t* d_in2,
+                  int64_t count, uint32_t* d_out, void* stream) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CU(cudaSetDevice(ctx->device));
+    return pbs_pipeline(ctx, nlut, lut_ids, in_boff, out_boff, d_in, d_in2, count, d_out, pick(ctx, stream));
+}
+
+int fdsnn_pbs_batch(fdsnn_ctx* ctx, int32_t lut_id, const int64_t* A, const int64_t* b,
+                    int64_t count, int64_t* outA, int64_t* outb) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CU(cudaSetDevice(ctx->device));
+    if (count <= 0) return FDSNN_OK;
+    int rc;
+    const size_t rb = (size_t)count * ctx->dp.stride * 4;
+    if ((rc = ctx->rows_a.ensure(rb)) || (rc = ctx->rows_b.ensure(rb))) return rc;
+    if ((rc = fdsnn_rows_from_host(ctx, A, b, count, (uint32_t*)ctx->rows_a.p, nullptr))) return rc;
+    if ((rc = pbs_pipeline(ctx, 1, &lut_id, nullptr, nullptr, (uint32_t*)ctx->rows_a.p, nullptr,
+                           count, (uint32_t*)ctx->rows_b.p, ctx->stream)))
+        return rc;
+    return fdsnn_rows_to_host(ctx, (uint32_t*)ctx->rows_b.p, count, outA, outb, nullptr);
+}
+
+int fdsnn_lif_step_batch(fdsnn_ctx* ctx, int32_t lut_fire, int32_t lut_reset, int64_t v_th_hat,
+                         const int64_t* vA, const int64_t* vb, const int64_t* iA, const int64_t* ib,
+                         int64_t count, int64_t* sA, int64_t* sb, int64_t* nA, int64_t* nb) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CU(cudaSetDevice(ctx->device));
+    if (count <= 0) return FDSNN_OK;
+    int rc;
+    const size_t rb = (size_t)count * ctx->dp.stride * 4;
+    if ((rc = ctx->rows_a.ensure(rb)) || (rc = ctx->rows_b.ensure(rb)) ||
+        (rc = ctx->rows_c.ensure(2 * rb)))
+        return rc;
+    uint32_t* rv = (uint32_t*)ctx->rows_a.p;
+    uint32_t* ri = (uint32_t*)ctx->rows_b.p;
+    uint32_t* ro = (uint32_t*)ctx->rows_c.p;
+    if ((rc = fdsnn_rows_from_host(ctx, vA, vb, count, rv, nullptr))) return rc;
+    // rows_from_host reuses the staging buffer: order the two uploads on the stream
+    if ((rc = fdsnn_rows_from_host(ctx, iA, ib, count, ri, nullptr))) return rc;
+    const int32_t luts[2] = {lut_fire, lut_reset};
+    const int64_t inb[2] = {-v_th_hat, 0};
+    const int64_t outb[2] = {1, 0};
+    if ((rc = pbs_pipeline(ctx, 2, luts, inb, outb, rv, ri, count, ro, ctx->stream))) return rc;
+    if ((rc = fdsnn_rows_to_host(ctx, ro, count, sA, sb, nullptr))) return rc;
+    return fdsnn_rows_to_host(ctx, ro + (size_t)count * ctx->dp.stride, count, nA, nb, nullptr);
+}
+
+int fdsnn_blind_rotate_batch(fdsnn_ctx* ctx, int64_t* acc, const int64_t* a2N, int64_t count) {
+    int rc;
+    if ((rc = check_keys(ctx))) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CU(cudaSetDevice(ctx->device));
+    if (count <= 0) return FDSNN_OK;
+    const DevParams& d = ctx->dp;
+    const size_t accn = (size_t)count * 2 * d.N, kn = (size_t)count * d.n;
+    std::vector<int32_t> h_acc(accn), h_k(kn);
+    for (size_t i = 0; i < accn; ++i) h_acc[i] = (int32_t)((uint32_t)acc[i] & d.qmask);
+    for (size_t i = 0; i < kn; ++i) h_k[i] = (int32_t)(((a2N[i] % (2 * d.N)) + 2 * d.N) % (2 * d.N));
+    if ((rc = ctx->acc_buf.ensure(accn * 4)) || (rc = ctx->a2n_buf.ensure(kn * 4))) return rc;
+    CU(cudaMemcpyAsync(ctx->acc_buf.p, h_acc.data(), accn * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->a2n_buf.p, h_k.data(), kn * 4, cudaMemcpyHostToDevice, ctx->stream));
+    PbsArgs a{};
+    a.prm = d;
+    a.count = count;
+    a.nlut = 1;
+    a.acc_io = (int32_t*)ctx->acc_buf.p;
+    a.a2N_in = (const int32_t*)ctx->a2n_buf.p;
+    a.bsk = ctx->bsk;
+    a.tables = ctx->tables;
+    a.margin = ctx->margin;
+    if ((rc = launch_br(ctx, a, count, true, ctx->stream))) return rc;
+    CU(cudaMemcpyAsync(h_acc.data(), ctx->acc_buf.p, accn * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (size_t i = 0; i < accn; ++i) acc[i] = (int64_t)(uint32_t)h_acc[i];
+    return FDSNN_OK;
+}
+
+int fdsnn_key_switch_batch(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b, int64_t count,
+                           int64_t* outA, int64_t* outb) {
+    int rc;
+    if ((rc = check_keys(ctx))) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CU(cudaSetDevice(ctx->device));
+    if (count <= 0) return FDSNN_OK;
+    const DevParams& d = ctx->dp;
+    std::vector<uint32_t> h((size_t)count * d.ext_stride, 0u);
+    for (int64_t r = 0; r < count; ++r) {
+        for (int j = 0; j < d.N; ++j) h[r * d.ext_stride + j] = (uint32_t)A[r * d.N + j] & d.qmask;
+        h[r * d.ext_stride + d.N] = (uint32_t)b[r] & d.qmask;
+    }
+    const size_t rb = (size_t)count * d.stride * 4;
+    if ((rc = ctx->ext.ensure(h.size() * 4)) || (rc = ctx->rows_b.ensure(rb))) return rc;
+    CU(cudaMemcpyAsync(ctx->ext.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    KsArgs k{};
+    k.prm = d;
+    k.ext = (const uint32_t*)ctx->ext.p;
+    k.V = count;
+    k.ksk = ctx->ksk;
+    k.out = (uint32_t*)ctx->rows_b.p;
+    k.count = count;
+    if ((rc = launch_ks(ctx, k, ctx->stream))) return rc;
+    return fdsnn_rows_to_host(ctx, (uint32_t*)ctx->rows_b.p, count, outA, outb, nullptr);
+}
+
+int fdsnn_operator_load(fdsnn_ctx* ctx, const int64_t* Mh, int64_t out_cells, int64_t in_cells,
+                        int32_t* op_id) {
+    if (!ctx || !Mh || !op_id) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+    if (out_cells <= 0 || in_cells <= 0 || out_cells > (1 << 30) || in_cells > (1 << 30))
+        return set_err(FDSNN_ERR_PARAMETER, "bad operator shape");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CU(cudaSetDevice(ctx->device));
+    Operator op;
+    op.out_cells = (int)out_cells;
+    op.in_cells = (int)in_cells;
+    int64_t nnz = 0;
+    const int64_t total = out_cells * in_cells;
+    for (int64_t i = 0; i < total; ++i) {
+        if (Mh[i] > INT32_MAX || Mh[i] < INT32_MIN)
+            return set_err(FDSNN_ERR_PARAMETER, "operator weight out of int32 range");
+        nnz += Mh[i] != 0;
+    }
+    op.dense = nnz * 4 > total;
+    if (op.dense) {
+        std::vector<int32_t> w((size_t)total);
+        for (int64_t i = 0; i < total; ++i) w[i] = (int32_t)Mh[i];
+        CU(cudaMalloc(&op.w, w.size() * 4));
+        CU(cudaMemcpy(op.w, w.data(), w.size() * 4, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<int32_t> rp(out_cells + 1), ci, va;
+        ci.reserve(nnz);
+        va.reserve(nnz);
+        for (int64_t r = 0; r < out_cells; ++r) {
+            rp[r] = (int32_t)ci.size();
+            for (int64_t c = 0; c < in_cells; ++c) {
+                const int64_t x = Mh[r * in_cells + c];
+                if (x) { ci.push_back((int32_t)c); va.push_back((int32_t)x); }
+            }
+        }
+        rp[out_cells] = (int32_t)ci.size();
+        CU(cudaMalloc(&op.row_ptr, rp.size() * 4));
+        CU(cudaMemcpy(op.row_ptr, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice));
+        const size_t nb = std::max<size_t>(1, ci.size()) * 4;
+        CU(cudaMalloc(&op.col_idx, nb));
+        CU(cudaMalloc(&op.val, nb));
+        if (!ci.empty()) {
+            CU(cudaMemcpy(op.col_idx, ci.data(), ci.size() * 4, cudaMemcpyHostToDevice));
+            CU(cudaMemcpy(op.val, va.data(), va.size() * 4, cudaMemcpyHostToDevice));
+        }
+    }
+    ctx->ops.push_back(op);
+    *op_id = (int32_t)ctx->ops.size() - 1;
+    return FDSNN_OK;
+}
+
+int fdsnn_operator_apply(fdsnn_ctx* ctx, int32_t op_id, const uint32_t* d_in, int64_t batch,
+                         uint32_t* d_out, void* stream) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    if (op_id < 0 || op_id >= (int32_t)ctx->ops.size()) return set_err(FDSNN_ERR_STATE, "unknown operator %d", op_id);
+    if (batch <= 0) return FDSNN_OK;
+    if (batch > 65535) return set_err(FDSNN_ERR_PARAMETER, "batch too large");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t s = pick(ctx, stream);
+    const Operator& op = ctx->ops[op_id];
+    const DevParams& d = ctx->dp;
+    TimerScope ts(ctx, 2, s);
+    if (op.dense) {
+        dim3 grid((op.out_cells + LIN_ROWS - 1) / LIN_ROWS, (d.stride + LIN_COLS - 1) / LIN_COLS, (unsigned)batch);
+        linear_dense_kernel<<<grid, 256, 0, s>>>(op.w, op.out_cells, op.in_cells, d_in, d_out, d.stride, d.qmask);
+    } else {
+        dim3 grid(op.out_cells, (unsigned)batch);
+        linear_csr_kernel<<<grid, 160, 0, s>>>(op.row_ptr, op.col_idx, op.val, op.out_cells, op.in_cells, d_in, d_out, d.stride, d.qmask);
+    }
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
+int fdsnn_weight_sum(fdsnn_ctx* ctx, const int64_t* Mh, int64_t out_cells, int64_t in_cells,
+                     const int64_t* A, const int64_t* b, int64_t* outA, int64_t* outb) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    int32_t id;
+    int rc;
+    if ((rc = fdsnn_operator_load(ctx, Mh, out_cells, in_cells, &id))) return rc;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    const DevParams& d = ctx->dp;
+    if ((rc = ctx->rows_a.ensure((size_t)in_cells * d.stride * 4)) ||
+        (rc = ctx->rows_b.ensure((size_t)out_cells * d.stride * 4)))
+        return rc;
+    if ((rc = fdsnn_rows_from_host(ctx, A, b, in_cells, (uint32_t*)ctx->rows_a.p, nullptr))) return rc;
+    if ((rc = fdsnn_operator_apply(ctx, id, (uint32_t*)ctx->rows_a.p, 1, (uint32_t*)ctx->rows_b.p, nullptr))) return rc;
+    rc = fdsnn_rows_to_host(ctx, (uint32_t*)ctx->rows_b.p, out_cells, outA, outb, nullptr);
+    // one-shot operator: release its device storage
+    Operator& op = ctx->ops[id];
+    cudaFree(op.w); cudaFree(op.row_ptr); cudaFree(op.col_idx); cudaFree(op.val);
+    op = Operator{};
+    return rc;
+}
+
+int fdsnn_rows_add(fdsnn_ctx* ctx, const uint32_t* d_x, const uint32_t* d_y, int64_t count,
+                   uint32_t* d_out, void* stream) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    if (count <= 0) return FDSNN_OK;
+    cudaStream_t s = pick(ctx, stream);
+    const int64_t words = count * ctx->dp.stride;
+    rows_add_kernel<<<grid1d(words), 256, 0, s>>>(d_x, d_y, d_out, words, ctx->dp.qmask);
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
+int fdsnn_dev_alloc(fdsnn_ctx* ctx, int64_t bytes, void** ptr) {
+    if (!ctx || !ptr) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaMalloc(ptr, (size_t)std::max<int64_t>(bytes, 4)));
+    return FDSNN_OK;
+}
+
+int fdsnn_dev_free(fdsnn_ctx* ctx, void* ptr) {
+    if (!ctx) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+    CU(cudaFree(ptr));
+    return FDSNN_OK;
+}
+
+int fdsnn_sync(fdsnn_ctx* ctx) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaDeviceSynchronize());
+    return FDSNN_OK;
+}
+
+int fdsnn_timing_enable(fdsnn_ctx* ctx, int32_t on) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    ctx->timing = on != 0;
+    return FDSNN_OK;
+}
+
+int fdsnn_timing_read(fdsnn_ctx* ctx, int32_t which, double* ms, int64_t* launches) {
+    if (!ctx || which < 0 || which > 2) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
+    for (auto& t : ctx->timed) {
+        CU(cudaEventSynchronize(t.b));
+        float e = 0.f;
+        CU(cudaEventElapsedTime(&e, t.a, t.b));
+        ctx->timed_ms[t.which] += e;
+        ctx->timed_n[t.which] += 1;
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+    }
+    ctx->timed.clear();
+    if (ms) *ms = ctx->timed_ms[which];
+    if (launches) *launches = ctx->timed_n[which];
+    return FDSNN_OK;
+}
+
+int fdsnn_timing_reset(fdsnn_ctx* ctx) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    double ms;
+    int64_t n;
+    fdsnn_timing_read(ctx, 0, &ms, &n);
+    for (int i = 0; i < 3; ++i) { ctx->timed_ms[i] = 0; ctx->timed_n[i] = 0; }
+    return FDSNN_OK;
+}
+
+int fdsnn_margin_enable(fdsnn_ctx* ctx, int32_t on) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    ctx->track_margin = on != 0;
+    CU(cudaMemset(ctx->margin, 0, sizeof(unsigned long long)));
+    return FDSNN_OK;
+}
+
+int fdsnn_margin_read(fdsnn_ctx* ctx, double* max_err) {
+    if (!ctx || !max_err) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
+    unsigned long long bits = 0;
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpy(&bits, ctx->margin, sizeof bits, cudaMemcpyDeviceToHost));
+    double v;
+    std::memcpy(&v, &bits, sizeof v);
+    *max_err = v;
+    return FDSNN_OK;
+}
+
+int fdsnn_probe_fp64_peak(fdsnn_ctx* ctx, double* tflops) {
+    if (!ctx || !tflops) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
+    CU(cudaSetDevice(ctx->device));
+    double* d = nullptr;
+    CU(cudaMalloc(&d, 8));
+    const int blocks = 148 * 8, threads = 256, iters = 2048;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    fp64_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(d, 64);  // warm-up
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(a, ctx->stream);
+        fp64_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(d, iters);
+        cudaEventRecord(b, ctx->stream);
+        CU(cudaEventSynchronize(b));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(d);
+    const double flops = 2.0 * 16 * 8 * (double)iters * blocks * threads;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    return FDSNN_OK;
+}
+
+int fdsnn_flush_l2(fdsnn_ctx* ctx, void* stream) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    const size_t bytes = 256ull << 20;  // 2x the 126 MB L2
+    int rc;
+    if ((rc = ctx->l2flush.ensure(bytes))) return rc;
+    CU(cudaMemsetAsync(ctx->l2flush.p, (int)(ctx->timed_n[0] & 0xff), bytes, pick(ctx, stream)));
+    return FDSNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,77 @@
+// common.cuh — shared device-side definitions for the fdsnn B200 kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define FDSNN_DEV __device__ __forceinline__
+
+// Parameter block passed by value to every kernel (mirrors params.FheParams,
+// reference params.py:36-106, restricted to the hot path).
+struct DevParams {
+    int n;          // LWE dimension
+    int N;          // ring degree
+    int M;          // N/2 complex points of the folded transform
+    int log2q;      // q = 2^log2q
+    uint32_t qmask; // q - 1
+    int bg_log;     // gadget base 2^bg_log
+    int L;          // gadget levels
+    int ks_log;     // key-switch base 2^ks_log
+    int ks_L;       // key-switch levels
+    int stride;     // LWE row stride in words (>= n+1, multiple of 4)
+    int ext_stride; // extracted z-LWE row stride (>= N+1, multiple of 4)
+    int p;          // message modulus
+    int half_slot;  // N / p (bootstrap.py:526 half-slot offset)
+};
+
+FDSNN_DEV double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+FDSNN_DEV double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// a * b
+FDSNN_DEV double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+FDSNN_DEV double2 cmulc(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+// acc += a * b
+FDSNN_DEV void cmac(double2& acc, double2 a, double2 b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
+}
+
+// Centered representative of x mod q in [-q/2, q/2) (ring.py:27-33).
+FDSNN_DEV int32_t center_q(uint32_t x, int log2q) {
+    uint32_t m = x & ((1u << log2q) - 1u);
+    return (m >= (1u << (log2q - 1))) ? (int32_t)(m - (1u << log2q)) : (int32_t)m;
+}
+
+// ring.rescale(x, q, 2N) (ring.py:56-67): round-half-away(centered(x)*2N/q) mod 2N.
+FDSNN_DEV uint32_t rescale_q_to_2N(uint32_t x, int log2q, int log2_2N) {
+    int32_t c = center_q(x, log2q);
+    int32_t r;
+    if (log2q >= log2_2N) {
+        int s = log2q - log2_2N;
+        if (s == 0) {
+            r = c;
+        } else {
+            int32_t mag = c < 0 ? -c : c;
+            int32_t t = (mag + (1 << (s - 1))) >> s;  // div_round_half_away (ring.py:45-53)
+            r = c < 0 ? -t : t;
+        }
+    } else {
+        r = c * (1 << (log2_2N - log2q));
+    }
+    return (uint32_t)r & ((1u << log2_2N) - 1u);
+}
+
+// round-half-away-from-zero exactly as ring.round_half_away (ring.py:36-42):
+// floor(x+0.5) for x>=0, ceil(x-0.5) otherwise.
+FDSNN_DEV long long round_half_away(double x) {
+    return (x >= 0.0) ? (long long)floor(x + 0.5) : (long long)ceil(x - 0.5);
+}
+
+FDSNN_DEV void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}

@@ -1,0 +1,180 @@
+// fft.cuh — register/shared-memory Stockham FFT for the folded negacyclic
+// transform of ring.NegacyclicTransform (reference ring.py:103-137).
+//
+// The reference evaluates a real length-N polynomial by folding it into
+// M = N/2 complex points c_j = (a_j + i a_{j+M}) * e^{i pi j / N} followed by a
+// length-M DFT with the e^{+2 pi i jk/M} kernel (scipy ifft, norm="forward"),
+// and inverts with the e^{-2 pi i} DFT, /M, untwist and unfold.
+//
+// B200 design: one polynomial is transformed by T = M/8 threads that each own
+// the 8 points {t + r*T : r < 8}.  A Stockham autosort formulation (natural
+// order in, natural order out) is used with radix-8 first and last passes, so
+//   * the first pass reads exactly the points the thread computed itself
+//     (digits of accumulator coefficients t + rT and t + rT + M),
+//   * the last forward pass leaves frequencies {t + rT} in registers, which is
+//     also the first inverse pass's input set -> the Fourier-domain MAC against
+//     the bootstrapping key and the hand-off to the inverse transform need no
+//     data exchange at all,
+//   * the last inverse pass leaves coefficients {t + rT, t + rT + M} in
+//     registers, i.e. exactly what the thread adds back into the accumulator.
+// Only the interior pass boundaries exchange data through shared memory
+// (padded a + a/8 to keep 16-byte accesses bank-conflict free).
+#pragma once
+#include "common.cuh"
+
+namespace fdsnn {
+
+// multiply by s*i where s = +1 (forward, e^{+}) or -1 (inverse)
+template <bool INV>
+FDSNN_DEV double2 mul_si(double2 a) {
+    return INV ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+}
+
+template <bool INV>
+FDSNN_DEV void dft2(double2& a, double2& b) {
+    double2 t = a;
+    a = cadd(t, b);
+    b = csub(t, b);
+}
+
+// 4-point DFT with kernel e^{s 2 pi i/4}, natural order in/out.
+template <bool INV>
+FDSNN_DEV void dft4(double2& y0, double2& y1, double2& y2, double2& y3) {
+    double2 c0 = cadd(y0, y2), c1 = csub(y0, y2);
+    double2 c2 = cadd(y1, y3), c3 = mul_si<INV>(csub(y1, y3));
+    y0 = cadd(c0, c2);
+    y2 = csub(c0, c2);
+    y1 = cadd(c1, c3);
+    y3 = csub(c1, c3);
+}
+
+// 8-point DFT with kernel e^{s 2 pi i/8}, natural order in/out.
+template <bool INV>
+FDSNN_DEV void dft8(double2* v) {
+    const double h = 0.70710678118654752440;  // sqrt(2)/2
+    double2 a0 = cadd(v[0], v[4]), b0 = csub(v[0], v[4]);
+    double2 a1 = cadd(v[1], v[5]), b1 = csub(v[1], v[5]);
+    double2 a2 = cadd(v[2], v[6]), b2 = csub(v[2], v[6]);
+    double2 a3 = cadd(v[3], v[7]), b3 = csub(v[3], v[7]);
+    // b1 *= e^{s i pi/4}, b2 *= s i, b3 *= e^{s 3 i pi/4}
+    if (!INV) {
+        b1 = make_double2(h * (b1.x - b1.y), h * (b1.y + b1.x));
+        b3 = make_double2(-h * (b3.x + b3.y), h * (b3.x - b3.y));
+    } else {
+        b1 = make_double2(h * (b1.x + b1.y), h * (b1.y - b1.x));
+        b3 = make_double2(h * (b3.y - b3.x), -h * (b3.x + b3.y));
+    }
+    b2 = mul_si<INV>(b2);
+    dft4<INV>(a0, a1, a2, a3);
+    dft4<INV>(b0, b1, b2, b3);
+    v[0] = a0; v[2] = a1; v[4] = a2; v[6] = a3;
+    v[1] = b0; v[3] = b1; v[5] = b2; v[7] = b3;
+}
+
+template <int R, bool INV>
+FDSNN_DEV void dftR(double2* v) {
+    if constexpr (R == 8) {
+        dft8<INV>(v);
+    } else if constexpr (R == 4) {
+        dft4<INV>(v[0], v[1], v[2], v[3]);
+    } else {
+        dft2<INV>(v[0], v[1]);
+    }
+}
+
+FDSNN_DEV int pad_idx(int a) { return a + (a >> 3); }
+
+// Pass schedule per transform size (product of radices = M; first and last 8).
+template <int M> struct Schedule;
+template <> struct Schedule<256> { static constexpr int P = 3; static constexpr int R[4] = {8, 4, 8, 0}; };
+template <> struct Schedule<512> { static constexpr int P = 3; static constexpr int R[4] = {8, 8, 8, 0}; };
+template <> struct Schedule<1024> { static constexpr int P = 4; static constexpr int R[4] = {8, 4, 4, 8}; };
+
+template <int M, int PASS>
+struct PassInfo {
+    static constexpr int R = Schedule<M>::R[PASS];
+    static constexpr int NS = PASS == 0 ? 1 : PassInfo<M, PASS - 1>::NS * PassInfo<M, PASS - 1>::R;
+};
+template <int M>
+struct PassInfo<M, -1> { static constexpr int R = 1; static constexpr int NS = 1; };
+
+// Group-local synchronisation handle for the T threads transforming one poly.
+struct GroupSync {
+    int bar_id;
+    int nthreads;
+    FDSNN_DEV void sync() const { named_bar(bar_id, nthreads); }
+};
+
+// One Stockham pass.  v holds 8/R independent R-point groups.  W is the
+// table e^{+2 pi i k / M}, k < M (in shared memory).
+template <int M, int PASS, bool INV>
+FDSNN_DEV void pass_body(double2 (&v)[8], int t, const double2* __restrict__ W) {
+    constexpr int T = M / 8;
+    constexpr int R = PassInfo<M, PASS>::R;
+    constexpr int NS = PassInfo<M, PASS>::NS;
+#pragma unroll
+    for (int s = 0; s < 8 / R; ++s) {
+        const int j = t + T * s;
+        if constexpr (NS > 1) {
+            const int jm = j % NS;
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                const double2 w = W[(r * jm) * (M / (NS * R))];
+                v[s * R + r] = INV ? cmulc(v[s * R + r], w) : cmul(v[s * R + r], w);
+            }
+        }
+        dftR<R, INV>(&v[s * R]);
+    }
+}
+
+template <int M, int PASS>
+FDSNN_DEV void pass_store(const double2 (&v)[8], int t, double2* __restrict__ buf) {
+    constexpr int T = M / 8;
+    constexpr int R = PassInfo<M, PASS>::R;
+    constexpr int NS = PassInfo<M, PASS>::NS;
+#pragma unroll
+    for (int s = 0; s < 8 / R; ++s) {
+        const int j = t + T * s;
+        const int idxD = (j / NS) * NS * R + (j % NS);
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[pad_idx(idxD + r * NS)] = v[s * R + r];
+    }
+}
+
+template <int M, int PASS>
+FDSNN_DEV void pass_load(double2 (&v)[8], int t, const double2* __restrict__ buf) {
+    constexpr int T = M / 8;
+    constexpr int R = PassInfo<M, PASS>::R;
+#pragma unroll
+    for (int s = 0; s < 8 / R; ++s) {
+        const int j = t + T * s;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[s * R + r] = buf[pad_idx(j + r * (M / R))];
+    }
+}
+
+// Full transform: v (points t + rT) -> v (frequencies t + rT).
+// `ex` is the running exchange parity (alternates the two exchange buffers so
+// that a single barrier per exchange is race free across consecutive FFTs).
+template <int M, bool INV>
+FDSNN_DEV void fft_group(double2 (&v)[8], int t, const double2* __restrict__ W,
+                         double2* __restrict__ buf0, double2* __restrict__ buf1,
+                         int& ex, const GroupSync& gs) {
+    constexpr int P = Schedule<M>::P;
+    pass_body<M, 0, INV>(v, t, W);
+#define FDSNN_FFT_STEP(PS)                                        \
+    if constexpr (PS < P) {                                       \
+        double2* b = ex ? buf1 : buf0;                            \
+        pass_store<M, PS - 1>(v, t, b);                           \
+        gs.sync();                                                \
+        pass_load<M, PS>(v, t, b);                                \
+        ex ^= 1;                                                  \
+        pass_body<M, PS, INV>(v, t, W);                           \
+    }
+    FDSNN_FFT_STEP(1)
+    FDSNN_FFT_STEP(2)
+    FDSNN_FFT_STEP(3)
+#undef FDSNN_FFT_STEP
+}
+
+}  // namespace fdsnn

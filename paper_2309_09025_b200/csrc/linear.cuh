@@ -1,0 +1,141 @@
+// linear.cuh — homomorphic weighted sums (network.layer_forward,
+// reference network.py:409-421): out = M @ [A | b] mod q for an integer
+// operator M (conv / pool / linear, all lowered to (out_cells, in_cells)).
+//
+// The reference computes the product in float64 (asserted exact, :417) and
+// reduces mod q.  Here: int32 multiply-accumulate with wrap-around mod 2^32,
+// exact modulo q = 2^k, on the uint32 row layout.  Two kernels:
+//   * dense tiled GEMM (fully connected layers), weight tile reused across a
+//     128-column ciphertext tile, ciphertext tile reused across 64 rows;
+//   * CSR gather (conv / pool lowered matrices are >95% zeros: 25 non-zeros
+//     per conv row), one CTA per output row, 16-byte column vectors.
+#pragma once
+#include "common.cuh"
+
+namespace fdsnn {
+
+constexpr int LIN_ROWS = 64;
+constexpr int LIN_COLS = 128;
+constexpr int LIN_K = 16;
+
+// Dense: Wm (out x in) int32 row-major; X batch-stacked rows (batch*in x stride)
+template <bool DUMMY = false>
+__global__ void __launch_bounds__(256)
+linear_dense_kernel(const int32_t* __restrict__ Wm, int out_cells, int in_cells,
+                    const uint32_t* __restrict__ X, uint32_t* __restrict__ Y,
+                    int stride, uint32_t qmask) {
+    __shared__ __align__(16) int32_t ws[LIN_K][LIN_ROWS];
+    __shared__ __align__(16) uint32_t xs[LIN_K][LIN_COLS];
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+    const int r0 = blockIdx.x * LIN_ROWS;
+    const int c0 = blockIdx.y * LIN_COLS;
+    const int bidx = blockIdx.z;
+    const uint32_t* Xb = X + (size_t)bidx * in_cells * stride;
+    uint32_t* Yb = Y + (size_t)bidx * out_cells * stride;
+    uint32_t acc[8][4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0u;
+    for (int k0 = 0; k0 < in_cells; k0 += LIN_K) {
+        for (int e = threadIdx.x; e < LIN_K * LIN_ROWS; e += blockDim.x) {
+            const int rr = e / LIN_K, kk = e % LIN_K;
+            const int r = r0 + rr, k = k0 + kk;
+            ws[kk][rr] = (r < out_cells && k < in_cells) ? Wm[(size_t)r * in_cells + k] : 0;
+        }
+        for (int e = threadIdx.x; e < LIN_K * (LIN_COLS / 4); e += blockDim.x) {
+            const int kk = e / (LIN_COLS / 4), cc = (e % (LIN_COLS / 4)) * 4;
+            const int k = k0 + kk, c = c0 + cc;
+            uint4 val = make_uint4(0, 0, 0, 0);
+            if (k < in_cells && c < stride)
+                val = *reinterpret_cast<const uint4*>(Xb + (size_t)k * stride + c);
+            *reinterpret_cast<uint4*>(&xs[kk][cc]) = val;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < LIN_K; ++kk) {
+            const int4 w0 = *reinterpret_cast<const int4*>(&ws[kk][ty * 8]);
+            const int4 w1 = *reinterpret_cast<const int4*>(&ws[kk][ty * 8 + 4]);
+            const uint4 xv = *reinterpret_cast<const uint4*>(&xs[kk][tx * 4]);
+            const int32_t wd[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+            const uint32_t xd[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] += (uint32_t)wd[a] * xd[b];
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const int r = r0 + ty * 8 + a;
+        if (r >= out_cells) continue;
+        const int c = c0 + tx * 4;
+        if (c < stride) {
+            uint4 o = make_uint4(acc[a][0] & qmask, acc[a][1] & qmask, acc[a][2] & qmask,
+                                 acc[a][3] & qmask);
+            *reinterpret_cast<uint4*>(Yb + (size_t)r * stride + c) = o;
+        }
+    }
+}
+
+// CSR: row_ptr (out+1), col_idx/val (nnz).  grid = (out_cells, batch).
+__global__ void __launch_bounds__(160)
+linear_csr_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                  const int32_t* __restrict__ val, int out_cells, int in_cells,
+                  const uint32_t* __restrict__ X, uint32_t* __restrict__ Y, int stride,
+                  uint32_t qmask) {
+    const int r = blockIdx.x;
+    const int bidx = blockIdx.y;
+    const uint32_t* Xb = X + (size_t)bidx * in_cells * stride;
+    uint32_t* Yb = Y + (size_t)bidx * out_cells * stride;
+    const int beg = row_ptr[r], end = row_ptr[r + 1];
+    for (int c = threadIdx.x * 4; c < stride; c += blockDim.x * 4) {
+        uint32_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+        for (int e = beg; e < end; ++e) {
+            const uint32_t w = (uint32_t)__ldg(val + e);
+            const uint4 xv = __ldg(reinterpret_cast<const uint4*>(Xb + (size_t)__ldg(col_idx + e) * stride + c));
+            s0 += w * xv.x; s1 += w * xv.y; s2 += w * xv.z; s3 += w * xv.w;
+        }
+        *reinterpret_cast<uint4*>(Yb + (size_t)r * stride + c) =
+            make_uint4(s0 & qmask, s1 & qmask, s2 & qmask, s3 & qmask);
+    }
+}
+
+__global__ void rows_add_kernel(const uint32_t* __restrict__ x, const uint32_t* __restrict__ y,
+                                uint32_t* __restrict__ out, int64_t words, uint32_t qmask) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (x[i] + y[i]) & qmask;
+}
+
+// int64 host-layout (A,b) -> uint32 rows (mod q); pad columns zeroed.
+__global__ void rows_pack_kernel(const int64_t* __restrict__ A, const int64_t* __restrict__ b,
+                                 int64_t count, int n, int stride, uint32_t qmask,
+                                 uint32_t* __restrict__ rows) {
+    const int64_t total = count * stride;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / stride;
+        const int c = (int)(i - r * stride);
+        uint32_t v = 0;
+        if (c < n) v = (uint32_t)(A[r * n + c]) & qmask;
+        else if (c == n) v = (uint32_t)(b[r]) & qmask;
+        rows[i] = v;
+    }
+}
+
+__global__ void rows_unpack_kernel(const uint32_t* __restrict__ rows, int64_t count, int n,
+                                   int stride, int64_t* __restrict__ A, int64_t* __restrict__ b) {
+    const int64_t total = count * (n + 1);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / (n + 1);
+        const int c = (int)(i - r * (n + 1));
+        const uint32_t v = rows[r * stride + c];
+        if (c < n) A[r * n + c] = (int64_t)v;
+        else b[r] = (int64_t)v;
+    }
+}
+
+}  // namespace fdsnn

@@ -1,0 +1,241 @@
+"""Device context: the Python face of one `fdsnn_ctx` (C ABI, include/fdsnn_b200.h).
+
+A context owns, on one B200, the Fourier-domain bootstrapping key (computed on
+the device from the integer RGSW rows), the key-switch key, the registered
+test polynomials and the integer weight operators.  Host-buffer calls
+(`pbs_batch`, `lif_step_batch`, ...) copy in and out inside the C library;
+device calls (`*_dev`) operate on device-resident ciphertext rows held in
+torch tensors (torch is used only as the device allocator / stream source).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import DeviceError, ParameterError
+from .params import FheParams
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _tptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _log2(x: int) -> int:
+    return int(x).bit_length() - 1
+
+
+class DeviceContext:
+    """Owns one C context; all methods raise DeviceError/ParameterError on failure."""
+
+    def __init__(self, params: FheParams, device: int = 0):
+        self.lib = _lib.load()
+        self.params = params
+        self.device = device
+        prm = _lib.FdsnnParams(params.n, params.N, _log2(params.q), params.p,
+                               params.gadget.log2_base, params.gadget.levels,
+                               _log2(params.ks_base), params.ks_levels)
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.fdsnn_ctx_create(ctypes.byref(prm), device, ctypes.byref(h)))
+        self.h = h
+        self.stride = int(self.lib.fdsnn_row_stride(params.n))
+        self._luts: dict[bytes, int] = {}
+        self._ops: dict[int, tuple] = {}
+        self.keys_loaded = False
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.fdsnn_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- keys
+    def load_keys(self, rows: np.ndarray, ksk_A: np.ndarray, ksk_b: np.ndarray) -> None:
+        p = self.params
+        rows = _i64(rows)
+        if rows.shape != (p.n, 2 * p.gadget.levels, 2, p.N):
+            raise ParameterError(f"RGSW rows shape {rows.shape} does not match params")
+        ksk_A, ksk_b = _i64(ksk_A), _i64(ksk_b)
+        if ksk_A.shape != (p.N * p.ks_levels, p.n) or ksk_b.shape != (p.N * p.ks_levels,):
+            raise ParameterError("key-switch key shape does not match params")
+        _lib.check(self.lib.fdsnn_bsk_load(self.h, _ptr(rows), _ptr(ksk_A), _ptr(ksk_b)))
+        self.keys_loaded = True
+
+    def lut(self, testpoly: np.ndarray) -> int:
+        tp = _i64(testpoly)
+        if tp.shape != (self.params.N,):
+            raise ParameterError("test polynomial must have N coefficients")
+        key = tp.tobytes()
+        lid = self._luts.get(key)
+        if lid is None:
+            out = ctypes.c_int32()
+            _lib.check(self.lib.fdsnn_lut_load(self.h, _ptr(tp), ctypes.byref(out)))
+            lid = self._luts[key] = int(out.value)
+        return lid
+
+    # ------------------------------------------------ host-buffer entry points
+    def pbs_batch(self, lut_id: int, A, b):
+        A, b = _i64(A), _i64(b)
+        cnt = len(b)
+        outA = np.empty((cnt, self.params.n), dtype=np.int64)
+        outb = np.empty(cnt, dtype=np.int64)
+        _lib.check(self.lib.fdsnn_pbs_batch(self.h, lut_id, _ptr(A), _ptr(b), cnt,
+                                            _ptr(outA), _ptr(outb)))
+        return outA, outb
+
+    def lif_step_batch(self, lut_fire: int, lut_reset: int, v_th_hat: int, vA, vb, iA, ib):
+        vA, vb, iA, ib = _i64(vA), _i64(vb), _i64(iA), _i64(ib)
+        cnt = len(vb)
+        n = self.params.n
+        out = [np.empty((cnt, n), np.int64), np.empty(cnt, np.int64),
+               np.empty((cnt, n), np.int64), np.empty(cnt, np.int64)]
+        _lib.check(self.lib.fdsnn_lif_step_batch(
+            self.h, lut_fire, lut_reset, int(v_th_hat), _ptr(vA), _ptr(vb), _ptr(iA), _ptr(ib),
+            cnt, *[_ptr(o) for o in out]))
+        return tuple(out)
+
+    def blind_rotate_batch(self, acc, a2N):
+        acc = _i64(acc).copy()
+        a2N = _i64(a2N)
+        _lib.check(self.lib.fdsnn_blind_rotate_batch(self.h, _ptr(acc), _ptr(a2N), acc.shape[0]))
+        return acc
+
+    def key_switch_batch(self, A, b):
+        A, b = _i64(A), _i64(b)
+        cnt = len(b)
+        outA = np.empty((cnt, self.params.n), np.int64)
+        outb = np.empty(cnt, np.int64)
+        _lib.check(self.lib.fdsnn_key_switch_batch(self.h, _ptr(A), _ptr(b), cnt,
+                                                   _ptr(outA), _ptr(outb)))
+        return outA, outb
+
+    def weight_sum(self, M, A, b):
+        M, A, b = _i64(M), _i64(A), _i64(b)
+        out_cells, in_cells = M.shape
+        outA = np.empty((out_cells, self.params.n), np.int64)
+        outb = np.empty(out_cells, np.int64)
+        _lib.check(self.lib.fdsnn_weight_sum(self.h, _ptr(M), out_cells, in_cells, _ptr(A),
+                                             _ptr(b), _ptr(outA), _ptr(outb)))
+        return outA, outb
+
+    # ------------------------------------------------- device-resident path
+    @staticmethod
+    def _torch():
+        import torch
+        if not torch.cuda.is_available():
+            raise DeviceError("CUDA device not available to torch")
+        return torch
+
+    def _stream(self):
+        torch = self._torch()
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def empty_rows(self, count: int):
+        torch = self._torch()
+        return torch.empty((max(count, 0), self.stride), dtype=torch.int32,
+                           device=f"cuda:{self.device}")
+
+    def zero_rows(self, count: int):
+        t = self.empty_rows(count)
+        t.zero_()
+        return t
+
+    def rows_from_host(self, A, b):
+        A, b = _i64(A), _i64(b)
+        rows = self.empty_rows(len(b))
+        _lib.check(self.lib.fdsnn_rows_from_host(self.h, _ptr(A), _ptr(b), len(b),
+                                                 _tptr(rows), self._stream()))
+        return rows
+
+    def rows_to_host(self, rows):
+        cnt = rows.shape[0]
+        A = np.empty((cnt, self.params.n), np.int64)
+        b = np.empty(cnt, np.int64)
+        _lib.check(self.lib.fdsnn_rows_to_host(self.h, _tptr(rows), cnt, _ptr(A), _ptr(b),
+                                               self._stream()))
+        return A, b
+
+    def pbs_dev(self, lut_ids, in_boff, out_boff, rows, rows2=None, out=None):
+        nl = len(lut_ids)
+        cnt = rows.shape[0]
+        if out is None:
+            out = self.empty_rows(nl * cnt)
+        ids = (ctypes.c_int32 * nl)(*[int(x) for x in lut_ids])
+        ib = (ctypes.c_int64 * nl)(*[int(x) for x in in_boff])
+        ob = (ctypes.c_int64 * nl)(*[int(x) for x in out_boff])
+        _lib.check(self.lib.fdsnn_pbs_dev(self.h, nl, ids, ib, ob, _tptr(rows), _tptr(rows2),
+                                          cnt, _tptr(out), self._stream()))
+        return out
+
+    def operator(self, matrix) -> int:
+        key = id(matrix)
+        hit = self._ops.get(key)
+        if hit is not None and hit[0] is matrix:
+            return hit[1]
+        M = _i64(matrix)
+        out = ctypes.c_int32()
+        _lib.check(self.lib.fdsnn_operator_load(self.h, _ptr(M), M.shape[0], M.shape[1],
+                                                ctypes.byref(out)))
+        self._ops[key] = (matrix, int(out.value))
+        return int(out.value)
+
+    def apply(self, op_id: int, rows, batch: int, out_cells: int, out=None):
+        if out is None:
+            out = self.empty_rows(batch * out_cells)
+        _lib.check(self.lib.fdsnn_operator_apply(self.h, op_id, _tptr(rows), batch, _tptr(out),
+                                                 self._stream()))
+        return out
+
+    def rows_add(self, x, y, out=None):
+        if out is None:
+            out = self.empty_rows(x.shape[0])
+        _lib.check(self.lib.fdsnn_rows_add(self.h, _tptr(x), _tptr(y), x.shape[0], _tptr(out),
+                                           self._stream()))
+        return out
+
+    # ------------------------------------------------------ instrumentation
+    def sync(self):
+        _lib.check(self.lib.fdsnn_sync(self.h))
+
+    def timing(self, on: bool):
+        _lib.check(self.lib.fdsnn_timing_enable(self.h, 1 if on else 0))
+
+    def timing_read(self, which: int):
+        ms = ctypes.c_double()
+        n = ctypes.c_int64()
+        _lib.check(self.lib.fdsnn_timing_read(self.h, which, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
+
+    def timing_reset(self):
+        _lib.check(self.lib.fdsnn_timing_reset(self.h))
+
+    def margin(self, on: bool | None = None):
+        if on is not None:
+            _lib.check(self.lib.fdsnn_margin_enable(self.h, 1 if on else 0))
+            return None
+        v = ctypes.c_double()
+        _lib.check(self.lib.fdsnn_margin_read(self.h, ctypes.byref(v)))
+        return v.value
+
+    def fp64_peak_tflops(self) -> float:
+        v = ctypes.c_double()
+        _lib.check(self.lib.fdsnn_probe_fp64_peak(self.h, ctypes.byref(v)))
+        return v.value
+
+    def flush_l2(self):
+        _lib.check(self.lib.fdsnn_flush_l2(self.h, self._stream()))

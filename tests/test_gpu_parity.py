@@ -1,0 +1,104 @@
+"""GPU parity: every device entry point vs the CPU oracle, bit-exact."""
+import numpy as np
+import pytest
+
+from conftest import O, oracle_key
+from paper_2309_09025_b200 import bootstrap, lwe, network, neuron
+
+pytestmark = pytest.mark.gpu
+
+
+def _enc(prm, sk, count, seed, lo=None, hi=None):
+    rng = np.random.default_rng(seed)
+    lo = -prm.p // 2 + 1 if lo is None else lo
+    hi = prm.p // 2 if hi is None else hi
+    ms = rng.integers(lo, hi + 1, count)
+    A, b = lwe.encrypt_batch(ms, sk, prm, rng)
+    return ms, A, b
+
+
+@pytest.mark.parametrize("which", ["toy", "toy64", "desk"])
+def test_bootstrap_batch_bit_exact(which, request):
+    prm = request.getfixturevalue(which)
+    sk, _, bsk = request.getfixturevalue(which + "_keys")
+    ms, A, b = _enc(prm, sk, 48, 11)
+    g = neuron.g_fire(prm.p)
+    outA, outb = bootstrap.bootstrap_batch(g, A, b, bsk)
+    key = oracle_key(prm, bsk)
+    wA, wb = O.bootstrap_batch(g.table, A, b, key)
+    assert np.array_equal(outA, wA) and np.array_equal(outb, wb)
+    assert np.array_equal(lwe.decrypt_batch(outA, outb, sk, prm), g(ms))
+
+
+def test_random_lut_and_counter(toy64, toy64_keys):
+    sk, _, bsk = toy64_keys
+    rng = np.random.default_rng(3)
+    g = bootstrap.make_program(dict(enumerate(rng.integers(-31, 33, 32))), toy64.p)
+    ms, A, b = _enc(toy64, sk, 64, 12)
+    before = bsk.bootstrap_count
+    outA, outb = bootstrap.bootstrap_batch(g, A, b, bsk)
+    assert bsk.bootstrap_count == before + 64
+    wA, wb = O.bootstrap_batch(g.table, A, b, oracle_key(toy64, bsk))
+    assert np.array_equal(outA, wA) and np.array_equal(outb, wb)
+
+
+def test_blind_rotate_batch(toy, toy_keys):
+    sk, zk, bsk = toy_keys
+    rng = np.random.default_rng(4)
+    acc = rng.integers(0, toy.q, (5, 2, toy.N))
+    a2N = rng.integers(0, 2 * toy.N, (5, toy.n))
+    a2N[0] = 0  # identity rotation
+    got = bootstrap.blind_rotate_batch(acc, a2N, bsk)
+    want = O.blind_rotate(acc, a2N, oracle_key(toy, bsk))
+    assert np.array_equal(got, want)
+
+
+def test_key_switch_batch(toy, toy_keys):
+    sk, zk, bsk = toy_keys
+    rng = np.random.default_rng(5)
+    A = rng.integers(-toy.q, toy.q, (9, toy.N))
+    b = rng.integers(0, toy.q, 9)
+    got = bootstrap.key_switch_batch(A, b, bsk.ksk, toy)
+    want = O.key_switch(A, b, oracle_key(toy, bsk))
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+@pytest.mark.parametrize("which", ["toy64", "desk"])
+def test_lif_step_bit_exact(which, request):
+    prm = request.getfixturevalue(which)
+    sk, _, bsk = request.getfixturevalue(which + "_keys")
+    lif = neuron.LifParams(tau=2, theta=max(1, prm.p // 16))
+    _, vA, vb = _enc(prm, sk, 40, 21, 0, lif.v_th_hat - 1)
+    _, iA, ib = _enc(prm, sk, 40, 22)
+    got = neuron.fhe_lif_step_batch(vA, vb, iA, ib, lif, bsk)
+    want = O.lif_step(vA, vb, iA, ib, lif.v_th_hat, lif.leak_num, lif.leak_den, oracle_key(prm, bsk))
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
+def test_c4_lif_step_bit_exact(c4prm, c4_keys):
+    sk, _, bsk = c4_keys
+    lif = neuron.LifParams(tau=2, theta=256)
+    _, iA, ib = _enc(c4prm, sk, 4, 23)
+    zA, zb = np.zeros_like(iA), np.zeros_like(ib)
+    got = neuron.fhe_lif_step_batch(zA, zb, iA, ib, lif, bsk)
+    want = O.lif_step(zA, zb, iA, ib, lif.v_th_hat, lif.leak_num, lif.leak_den, oracle_key(c4prm, bsk))
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
+@pytest.mark.parametrize("dense", [True, False])
+def test_layer_forward(desk, desk_keys, dense):
+    sk, _, _ = desk_keys
+    rng = np.random.default_rng(6)
+    if dense:
+        M = rng.integers(-15, 16, (37, 50))
+        shape = (37,)
+    else:
+        w = rng.integers(-7, 8, (3, 1, 3, 3))
+        M, shape = network.conv_matrix(w, (1, 5, 10), (1, 1), (0, 0))
+    ms, A, b = _enc(desk, sk, M.shape[1], 7, 0, 1)
+    layer = network.WeightLayer("linear", M, None, 1.0, shape)
+    out = network.layer_forward(network.CiphertextTensor((M.shape[1],), A, b, desk.q), layer, desk)
+    wA, wb = O.layer_forward(M, A, b, desk.q)
+    assert np.array_equal(out.A, wA) and np.array_equal(out.b, wb)
