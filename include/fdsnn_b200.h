@@ -106,7 +106,7 @@ int fdsnn_weight_sum(fdsnn_ctx* ctx, const int64_t* M, int64_t out_cells,
 
 /* ---- device-pointer entry points (device-resident pipeline) ----------- */
 /* All `rows` pointers are uint32 device arrays of count * fdsnn_row_stride(n)
- * words.  `stream` may be NULL (context stream). */
+ * words.  `stream` may be NULL: the legacy default stream. */
 
 /* Host int64 (A,b) -> device rows (with mod-q masking) and back. */
 int fdsnn_rows_from_host(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b,

@@ -120,8 +120,11 @@ struct TimerScope {
     }
 };
 
+// NULL selects the legacy default stream (torch's default stream), so device
+// entry points order naturally with the caller's other work.
 cudaStream_t pick(fdsnn_ctx* ctx, void* stream) {
-    return stream ? reinterpret_cast<cudaStream_t>(stream) : ctx->stream;
+    (void)ctx;
+    return stream ? reinterpret_cast<cudaStream_t>(stream) : cudaStreamLegacy;
 }
 
 template <int M, int G, bool RAW, bool MARGIN>
@@ -147,9 +150,9 @@ int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_
     if (V <= 0) return FDSNN_OK;
     TimerScope ts(ctx, 0, s);
     switch (ctx->dp.M) {
-        case 256: return launch_br_m<256, 4>(ctx, a, V, raw, s);
-        case 512: return launch_br_m<512, 2>(ctx, a, V, raw, s);
-        case 1024: return launch_br_m<1024, 1>(ctx, a, V, raw, s);
+        case 256: return launch_br_m<256, 8>(ctx, a, V, raw, s);
+        case 512: return launch_br_m<512, 4>(ctx, a, V, raw, s);
+        case 1024: return launch_br_m<1024, 2>(ctx, a, V, raw, s);
     }
     return set_err(FDSNN_ERR_PARAMETER, "unsupported ring degree N=%d", ctx->dp.N);
 }
@@ -304,17 +307,29 @@ int fdsnn_ctx_create(const fdsnn_params* prm, int32_t device, fdsnn_ctx** out) {
         delete ctx;
         return set_err(FDSNN_ERR_CUDA, "stream creation failed");
     }
-    // transform tables in long double: W[k] = e^{2 pi i k/M}, twist[j] = e^{i pi j/N},
-    // untw[j] = conj(twist[j]) / M   (ring.py:115-118, bootstrap.py:432-436)
+    // transform tables in long double (ring.py:115-118):
+    //   twist[j] = e^{i pi j/N}, j < M, then the interior-pass twiddles
+    //   e^{2 pi i r jm/(NS R)} in the fft.cuh layout [pass][r-1][jm].
     const int M = d.M;
-    std::vector<double2> tab(3 * M);
     const long double PI = 3.141592653589793238462643383279502884L;
+    std::vector<double2> tab(M);
     for (int k = 0; k < M; ++k) {
-        long double ang = 2.0L * PI * k / M;
-        tab[k] = make_double2((double)cosl(ang), (double)sinl(ang));
         long double tw = PI * k / p.N;
-        tab[M + k] = make_double2((double)cosl(tw), (double)sinl(tw));
-        tab[2 * M + k] = make_double2((double)(cosl(tw) / M), (double)(-sinl(tw) / M));
+        tab[k] = make_double2((double)cosl(tw), (double)sinl(tw));
+    }
+    {
+        const int* radix = M == 256 ? Schedule<256>::R : M == 512 ? Schedule<512>::R : Schedule<1024>::R;
+        const int P = M == 1024 ? 4 : 3;
+        int ns = radix[0];
+        for (int pass = 1; pass < P; ++pass) {
+            const int R = radix[pass];
+            for (int r = 1; r < R; ++r)
+                for (int jm = 0; jm < ns; ++jm) {
+                    long double ang = 2.0L * PI * r * jm / ((long double)ns * R);
+                    tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+                }
+            ns *= R;
+        }
     }
     if (cudaMalloc(&ctx->tables, tab.size() * sizeof(double2)) != cudaSuccess ||
         cudaMemcpy(ctx->tables, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -362,7 +377,7 @@ int fdsnn_bsk_load(fdsnn_ctx* ctx, const int64_t* rows, const int64_t* ksk_A, co
         const int M = d.M;
         const int T = M / 8;
         const int G = 128 / T > 0 ? 128 / T : 1;
-        const size_t smem = 3 * (size_t)M * sizeof(double2) + (size_t)G * 2 * (M + M / 8) * sizeof(double2);
+        const size_t smem = (size_t)G * 2 * (M + M / 8) * sizeof(double2);
         const unsigned blocks = (unsigned)((npoly + G - 1) / G);
         switch (M) {
             case 256:
@@ -464,11 +479,11 @@ int fdsnn_pbs_batch(fdsnn_ctx* ctx, int32_t lut_id, const int64_t* A, const int6
     int rc;
     const size_t rb = (size_t)count * ctx->dp.stride * 4;
     if ((rc = ctx->rows_a.ensure(rb)) || (rc = ctx->rows_b.ensure(rb))) return rc;
-    if ((rc = fdsnn_rows_from_host(ctx, A, b, count, (uint32_t*)ctx->rows_a.p, nullptr))) return rc;
+    if ((rc = fdsnn_rows_from_host(ctx, A, b, count, (uint32_t*)ctx->rows_a.p, ctx->stream))) return rc;
     if ((rc = pbs_pipeline(ctx, 1, &lut_id, nullptr, nullptr, (uint32_t*)ctx->rows_a.p, nullptr,
                            count, (uint32_t*)ctx->rows_b.p, ctx->stream)))
         return rc;
-    return fdsnn_rows_to_host(ctx, (uint32_t*)ctx->rows_b.p, count, outA, outb, nullptr);
+    return fdsnn_rows_to_host(ctx, (uint32_t*)ctx->rows_b.p, count, outA, outb, ctx->stream);
 }
 
 int fdsnn_lif_step_batch(fdsnn_ctx* ctx, int32_t lut_fire, int32_t lut_reset, int64_t v_th_hat,
@@ -486,15 +501,15 @@ int fdsnn_lif_step_batch(fdsnn_ctx* ctx, int32_t lut_fire, int32_t lut_reset, in
     uint32_t* rv = (uint32_t*)ctx->rows_a.p;
     uint32_t* ri = (uint32_t*)ctx->rows_b.p;
     uint32_t* ro = (uint32_t*)ctx->rows_c.p;
-    if ((rc = fdsnn_rows_from_host(ctx, vA, vb, count, rv, nullptr))) return rc;
+    if ((rc = fdsnn_rows_from_host(ctx, vA, vb, count, rv, ctx->stream))) return rc;
     // rows_from_host reuses the staging buffer: order the two uploads on the stream
-    if ((rc = fdsnn_rows_from_host(ctx, iA, ib, count, ri, nullptr))) return rc;
+    if ((rc = fdsnn_rows_from_host(ctx, iA, ib, count, ri, ctx->stream))) return rc;
     const int32_t luts[2] = {lut_fire, lut_reset};
     const int64_t inb[2] = {-v_th_hat, 0};
     const int64_t outb[2] = {1, 0};
     if ((rc = pbs_pipeline(ctx, 2, luts, inb, outb, rv, ri, count, ro, ctx->stream))) return rc;
-    if ((rc = fdsnn_rows_to_host(ctx, ro, count, sA, sb, nullptr))) return rc;
-    return fdsnn_rows_to_host(ctx, ro + (size_t)count * ctx->dp.stride, count, nA, nb, nullptr);
+    if ((rc = fdsnn_rows_to_host(ctx, ro, count, sA, sb, ctx->stream))) return rc;
+    return fdsnn_rows_to_host(ctx, ro + (size_t)count * ctx->dp.stride, count, nA, nb, ctx->stream);
 }
 
 int fdsnn_blind_rotate_batch(fdsnn_ctx* ctx, int64_t* acc, const int64_t* a2N, int64_t count) {
@@ -551,7 +566,7 @@ int fdsnn_key_switch_batch(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b, i
     k.out = (uint32_t*)ctx->rows_b.p;
     k.count = count;
     if ((rc = launch_ks(ctx, k, ctx->stream))) return rc;
-    return fdsnn_rows_to_host(ctx, (uint32_t*)ctx->rows_b.p, count, outA, outb, nullptr);
+    return fdsnn_rows_to_host(ctx, (uint32_t*)ctx->rows_b.p, count, outA, outb, ctx->stream);
 }
 
 int fdsnn_operator_load(fdsnn_ctx* ctx, const int64_t* Mh, int64_t out_cells, int64_t in_cells,
@@ -637,9 +652,9 @@ int fdsnn_weight_sum(fdsnn_ctx* ctx, const int64_t* Mh, int64_t out_cells, int64
     if ((rc = ctx->rows_a.ensure((size_t)in_cells * d.stride * 4)) ||
         (rc = ctx->rows_b.ensure((size_t)out_cells * d.stride * 4)))
         return rc;
-    if ((rc = fdsnn_rows_from_host(ctx, A, b, in_cells, (uint32_t*)ctx->rows_a.p, nullptr))) return rc;
-    if ((rc = fdsnn_operator_apply(ctx, id, (uint32_t*)ctx->rows_a.p, 1, (uint32_t*)ctx->rows_b.p, nullptr))) return rc;
-    rc = fdsnn_rows_to_host(ctx, (uint32_t*)ctx->rows_b.p, out_cells, outA, outb, nullptr);
+    if ((rc = fdsnn_rows_from_host(ctx, A, b, in_cells, (uint32_t*)ctx->rows_a.p, ctx->stream))) return rc;
+    if ((rc = fdsnn_operator_apply(ctx, id, (uint32_t*)ctx->rows_a.p, 1, (uint32_t*)ctx->rows_b.p, ctx->stream))) return rc;
+    rc = fdsnn_rows_to_host(ctx, (uint32_t*)ctx->rows_b.p, out_cells, outA, outb, ctx->stream);
     // one-shot operator: release its device storage
     Operator& op = ctx->ops[id];
     cudaFree(op.w); cudaFree(op.row_ptr); cudaFree(op.col_idx); cudaFree(op.val);

@@ -56,19 +56,23 @@ FDSNN_DEV void dft8(double2* v) {
     double2 a1 = cadd(v[1], v[5]), b1 = csub(v[1], v[5]);
     double2 a2 = cadd(v[2], v[6]), b2 = csub(v[2], v[6]);
     double2 a3 = cadd(v[3], v[7]), b3 = csub(v[3], v[7]);
-    // b1 *= e^{s i pi/4}, b2 *= s i, b3 *= e^{s 3 i pi/4}
-    if (!INV) {
-        b1 = make_double2(h * (b1.x - b1.y), h * (b1.y + b1.x));
-        b3 = make_double2(-h * (b3.x + b3.y), h * (b3.x - b3.y));
-    } else {
-        b1 = make_double2(h * (b1.x + b1.y), h * (b1.y - b1.x));
-        b3 = make_double2(h * (b3.y - b3.x), -h * (b3.x + b3.y));
-    }
+    // odd outputs = DFT4(b0, b1 e^{s i pi/4}, b2 (s i), b3 e^{s 3i pi/4}).  The
+    // sqrt(2)/2 of the two diagonal twiddles is folded into the final FMAs:
+    // u1 = (1 + s i) b1, u3 = (-1 + s i) b3 cost additions only.
+    const double2 u1 = INV ? make_double2(b1.x + b1.y, b1.y - b1.x)
+                           : make_double2(b1.x - b1.y, b1.y + b1.x);
+    const double2 u3 = INV ? make_double2(b3.y - b3.x, -(b3.y + b3.x))
+                           : make_double2(-(b3.x + b3.y), b3.x - b3.y);
     b2 = mul_si<INV>(b2);
     dft4<INV>(a0, a1, a2, a3);
-    dft4<INV>(b0, b1, b2, b3);
     v[0] = a0; v[2] = a1; v[4] = a2; v[6] = a3;
-    v[1] = b0; v[3] = b1; v[5] = b2; v[7] = b3;
+    const double2 c0 = cadd(b0, b2), c1 = csub(b0, b2);
+    const double2 e = cadd(u1, u3);
+    const double2 f = mul_si<INV>(csub(u1, u3));
+    v[1] = make_double2(fma(h, e.x, c0.x), fma(h, e.y, c0.y));
+    v[5] = make_double2(fma(-h, e.x, c0.x), fma(-h, e.y, c0.y));
+    v[3] = make_double2(fma(h, f.x, c1.x), fma(h, f.y, c1.y));
+    v[7] = make_double2(fma(-h, f.x, c1.x), fma(-h, f.y, c1.y));
 }
 
 template <int R, bool INV>
@@ -105,21 +109,56 @@ struct GroupSync {
     FDSNN_DEV void sync() const { named_bar(bar_id, nthreads); }
 };
 
-// One Stockham pass.  v holds 8/R independent R-point groups.  W is the
-// table e^{+2 pi i k / M}, k < M (in shared memory).
+// Per-thread twiddle factors: for pass p >= 1 the thread's groups all share
+// jm = t mod NS_p (T is a multiple of NS_p for every interior pass), so each
+// pass needs R_p - 1 constants e^{2 pi i r jm/(NS_p R_p)}.  They are loaded
+// once per kernel into registers (no shared-memory traffic, no bank conflicts).
+template <int M>
+struct Twiddles {
+    double2 w[4][7];
+};
+
+// Host/device table layout: for pass p (1..P-1), entries [r-1][jm], jm < NS_p.
+template <int M>
+__host__ __device__ constexpr int twiddle_offset(int pass) {
+    int off = 0;
+    for (int p = 1; p < pass; ++p) {
+        int ns = 1;
+        for (int k = 0; k < p; ++k) ns *= Schedule<M>::R[k];
+        off += (Schedule<M>::R[p] - 1) * ns;
+    }
+    return off;
+}
+template <int M>
+__host__ __device__ constexpr int twiddle_table_size() { return twiddle_offset<M>(Schedule<M>::P); }
+
+template <int M, int PASS>
+FDSNN_DEV void load_twiddles_pass(Twiddles<M>& tw, int t, const double2* __restrict__ tab) {
+    if constexpr (PASS < Schedule<M>::P) {
+        constexpr int R = PassInfo<M, PASS>::R;
+        constexpr int NS = PassInfo<M, PASS>::NS;
+        const double2* base = tab + twiddle_offset<M>(PASS);
+#pragma unroll
+        for (int r = 1; r < R; ++r) tw.w[PASS][r - 1] = __ldg(base + (r - 1) * NS + (t % NS));
+        load_twiddles_pass<M, PASS + 1>(tw, t, tab);
+    }
+}
+template <int M>
+FDSNN_DEV void load_twiddles(Twiddles<M>& tw, int t, const double2* __restrict__ tab) {
+    load_twiddles_pass<M, 1>(tw, t, tab);
+}
+
+// One Stockham pass.  v holds 8/R independent R-point groups.
 template <int M, int PASS, bool INV>
-FDSNN_DEV void pass_body(double2 (&v)[8], int t, const double2* __restrict__ W) {
-    constexpr int T = M / 8;
+FDSNN_DEV void pass_body(double2 (&v)[8], const Twiddles<M>& tw) {
     constexpr int R = PassInfo<M, PASS>::R;
     constexpr int NS = PassInfo<M, PASS>::NS;
 #pragma unroll
     for (int s = 0; s < 8 / R; ++s) {
-        const int j = t + T * s;
         if constexpr (NS > 1) {
-            const int jm = j % NS;
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                const double2 w = W[(r * jm) * (M / (NS * R))];
+                const double2 w = tw.w[PASS][r - 1];
                 v[s * R + r] = INV ? cmulc(v[s * R + r], w) : cmul(v[s * R + r], w);
             }
         }
@@ -157,11 +196,11 @@ FDSNN_DEV void pass_load(double2 (&v)[8], int t, const double2* __restrict__ buf
 // `ex` is the running exchange parity (alternates the two exchange buffers so
 // that a single barrier per exchange is race free across consecutive FFTs).
 template <int M, bool INV>
-FDSNN_DEV void fft_group(double2 (&v)[8], int t, const double2* __restrict__ W,
+FDSNN_DEV void fft_group(double2 (&v)[8], int t, const Twiddles<M>& tw,
                          double2* __restrict__ buf0, double2* __restrict__ buf1,
                          int& ex, const GroupSync& gs) {
     constexpr int P = Schedule<M>::P;
-    pass_body<M, 0, INV>(v, t, W);
+    pass_body<M, 0, INV>(v, tw);
 #define FDSNN_FFT_STEP(PS)                                        \
     if constexpr (PS < P) {                                       \
         double2* b = ex ? buf1 : buf0;                            \
@@ -169,7 +208,7 @@ FDSNN_DEV void fft_group(double2 (&v)[8], int t, const double2* __restrict__ W,
         gs.sync();                                                \
         pass_load<M, PS>(v, t, b);                                \
         ex ^= 1;                                                  \
-        pass_body<M, PS, INV>(v, t, W);                           \
+        pass_body<M, PS, INV>(v, tw);                             \
     }
     FDSNN_FFT_STEP(1)
     FDSNN_FFT_STEP(2)

@@ -15,6 +15,11 @@
 // of (X^k - 1)*ACC, a register-resident MAC against the Fourier-domain key
 // slice, 2 inverse transforms, round and add back.  The accumulator never
 // leaves shared memory until the final sample extraction.
+//
+// Register-resident constants per thread: the twist e^{i pi p/N} of its 8
+// points and the interior-pass twiddles (fft.cuh Twiddles).  The device
+// Fourier key is pre-scaled by 1/M (exact: M is a power of two), so the
+// untwist of the inverse transform is a plain multiply by conj(twist).
 #pragma once
 #include "fft.cuh"
 
@@ -32,9 +37,9 @@ struct PbsArgs {
     // input mode B: raw accumulators + rotation indices (blind_rotate_batch)
     int32_t* acc_io;       // count x 2 x N
     const int32_t* a2N_in; // count x n
-    // key
-    const double2* bsk;    // (n, 2L, 2, M) Fourier-domain RGSW rows
-    // tables (global, copied to smem): W[M] = e^{2 pi i k/M}, twist[M], untw[M]=conj(twist)/M
+    // key: (n, 2L, 2, M) Fourier-domain RGSW rows, scaled by 1/M
+    const double2* bsk;
+    // tables: twist[M] | interior twiddles (fft.cuh layout)
     const double2* tables;
     // output mode A: extracted z-LWE rows (virtual ct v at v*ext_stride)
     uint32_t* ext_out;
@@ -47,50 +52,87 @@ struct PbsShape {
     static constexpr int PADM = M + M / 8;
 };
 
-// shared-memory bytes for G groups
+template <int M>
+__host__ __device__ constexpr size_t pbs_group_bytes(int N, int n) {
+    return 2 * PbsShape<M>::PADM * sizeof(double2)               // exchange buffers
+           + 2 * (size_t)N * sizeof(int32_t)                     // accumulator
+           + (((size_t)n * sizeof(uint16_t) + 15) & ~(size_t)15);  // a2N
+}
+
+// CTA = 256 threads = G groups of T = M/8; the key slice of each CMux step is
+// streamed through a ring of S stages by the TMA engine (cp.async.bulk), one
+// stage per (step, digit) chunk = 2 output polys x M complex = 32*M bytes,
+// shared by all G accumulators of the CTA.
+constexpr int PBS_THREADS = 256;
+template <int M> struct PbsRing { static constexpr int S = (M == 1024) ? 3 : 4; };
+template <int M>
+__host__ __device__ constexpr size_t pbs_chunk_bytes() { return (size_t)2 * M * sizeof(double2); }
+
 template <int M>
 __host__ __device__ constexpr size_t pbs_smem_bytes(int G, int N, int n) {
-    return (size_t)3 * M * sizeof(double2)                               // W, twist, untw
-           + (size_t)G * (2 * PbsShape<M>::PADM * sizeof(double2)       // exchange buffers
-                          + 2 * (size_t)N * sizeof(int32_t)             // accumulator
-                          + (((size_t)n * sizeof(uint16_t) + 15) & ~(size_t)15));  // a2N
+    return 128 + (size_t)PbsRing<M>::S * pbs_chunk_bytes<M>() + (size_t)G * pbs_group_bytes<M>(N, n);
+}
+
+template <int M>
+FDSNN_DEV void load_twist(double2 (&tw)[8], int t, const double2* __restrict__ tables) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) tw[r] = __ldg(tables + t + r * (M / 8));
 }
 
 template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN>
-__global__ void __launch_bounds__(G * (M / 8))
+__global__ void __launch_bounds__(PBS_THREADS, 1)
 pbs_blind_rotate_kernel(const PbsArgs args) {
+    static_assert(G * (M / 8) == PBS_THREADS, "CTA shape");
     constexpr int T = M / 8;
     constexpr int PADM = PbsShape<M>::PADM;
+    constexpr int S = PbsRing<M>::S;
+    constexpr uint32_t CHUNK = (uint32_t)pbs_chunk_bytes<M>();
     const DevParams& prm = args.prm;
-    const int N = 2 * M;
+    constexpr int N = 2 * M;
     const int n = prm.n;
     const int L = prm.L;
     const uint32_t qmask = prm.qmask;
-    const int log2_2N = __ffs(2 * N) - 1;
+    constexpr int log2_2N = (M == 256) ? 10 : (M == 512) ? 11 : 12;
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2* W = reinterpret_cast<double2*>(smem_raw);
-    double2* twist = W + M;
-    double2* untw = twist + M;
-    unsigned char* gbase = reinterpret_cast<unsigned char*>(untw + M);
-    const size_t gbytes = 2 * PADM * sizeof(double2) + 2 * (size_t)N * sizeof(int32_t) +
-                          (((size_t)n * sizeof(uint16_t) + 15) & ~(size_t)15);
-
-    for (int k = threadIdx.x; k < 3 * M; k += blockDim.x) W[k] = args.tables[k];
-
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+    uint64_t* empty = full + S;
+    double2* ring = reinterpret_cast<double2*>(smem_raw + 128);
     const int g = threadIdx.x / T;
     const int t = threadIdx.x % T;
-    unsigned char* mine = gbase + g * gbytes;
+    unsigned char* mine = smem_raw + 128 + S * CHUNK + g * pbs_group_bytes<M>(N, n);
     double2* buf0 = reinterpret_cast<double2*>(mine);
     double2* buf1 = buf0 + PADM;
     int32_t* acc = reinterpret_cast<int32_t*>(buf1 + PADM);  // [2][N]
     uint16_t* a2N = reinterpret_cast<uint16_t*>(acc + 2 * N);
-    __syncthreads();
 
     const int64_t V = (int64_t)args.nlut * args.count;
-    const int64_t v = (int64_t)blockIdx.x * G + g;
-    if (v >= V) return;  // only group barriers below
+    const int64_t v0 = (int64_t)blockIdx.x * G;
+    const int nact = (int)((V - v0) < G ? (V - v0) : G);  // active groups in this CTA
+    const int64_t nchunks = (int64_t)n * 2 * L;
+    const bool producer = threadIdx.x == 0;
+    if (producer) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], nact * T);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (producer) {
+        for (int s = 0; s < S && s < nchunks; ++s) {
+            mbar_arrive_expect_tx(&full[s], CHUNK);
+            bulk_g2s(ring + (size_t)s * 2 * M, args.bsk + (size_t)s * 2 * M, CHUNK, &full[s]);
+        }
+    }
+    if (g >= nact) return;  // only group barriers / mbarriers are used below
+    const int64_t v = v0 + g;
     const GroupSync gs{1 + g, T};
+
+    Twiddles<M> tw;
+    load_twiddles<M>(tw, t, args.tables + M);
+    double2 twist[8];
+    load_twist<M>(twist, t, args.tables);
 
     // ---------------- setup: modulus switch + accumulator init -------------
     if constexpr (!MODE_RAW) {
@@ -122,23 +164,39 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     }
     gs.sync();
 
-    // per-thread constant tables for its 8 points p_r = t + r*T
     const int bg = prm.bg_log;
     const int32_t halfB1 = (1 << (bg - 1)) - 1;  // B/2 - 1
     const int32_t bmask = (1 << bg) - 1;
     int ex = 0;
     double err_max = 0.0;
 
+    // release chunk c (all threads), and as producer refill its stage with c+S
+    auto release = [&](int64_t c) {
+        const int s = (int)(c % S);
+        mbar_arrive(&empty[s]);
+        if (producer && c + S < nchunks) {
+            mbar_wait(&empty[s], (uint32_t)((c / S) & 1));
+            mbar_arrive_expect_tx(&full[s], CHUNK);
+            bulk_g2s(ring + (size_t)s * 2 * M, args.bsk + (size_t)(c + S) * 2 * M, CHUNK, &full[s]);
+        }
+    };
+
+    int64_t c = 0;  // chunk counter = i * 2L + digit
     for (int i = 0; i < n; ++i) {
         const int k = a2N[i];
-        if (k == 0) continue;  // X^0*ACC - ACC = 0: the step is the identity
+        if (k == 0) {  // X^0*ACC - ACC = 0: identity step; keep the key ring in sync
+            for (int d = 0; d < 2 * L; ++d, ++c) {
+                mbar_wait(&full[c % S], (uint32_t)((c / S) & 1));
+                release(c);
+            }
+            continue;
+        }
         double2 O0[8], O1[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) O0[r] = O1[r] = make_double2(0.0, 0.0);
 
-        const double2* key_i = args.bsk + (size_t)i * (2 * L) * 2 * M;
-        for (int c = 0; c < 2; ++c) {
-            const int32_t* a = acc + c * N;
+        for (int cc = 0; cc < 2; ++cc) {
+            const int32_t* a = acc + cc * N;
             int32_t xlo[8], xhi[8];
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
@@ -152,7 +210,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     if (half == 0) xlo[r] = xc; else xhi[r] = xc;
                 }
             }
-            for (int lvl = 0; lvl < L; ++lvl) {
+            for (int lvl = 0; lvl < L; ++lvl, ++c) {
                 double2 vv[8];
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
@@ -160,29 +218,29 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     const int32_t d2 = ((xhi[r] + halfB1) & bmask) - halfB1;
                     xlo[r] = (xlo[r] - d1) >> bg;
                     xhi[r] = (xhi[r] - d2) >> bg;
-                    vv[r] = cmul(make_double2((double)d1, (double)d2), twist[t + r * T]);
+                    vv[r] = cmul(make_double2((double)d1, (double)d2), twist[r]);
                 }
-                fft_group<M, false>(vv, t, W, buf0, buf1, ex, gs);
-                const double2* kd = key_i + (size_t)(c * L + lvl) * 2 * M;
+                fft_group<M, false>(vv, t, tw, buf0, buf1, ex, gs);
+                const int s = (int)(c % S);
+                mbar_wait(&full[s], (uint32_t)((c / S) & 1));
+                const double2* kd = ring + (size_t)s * 2 * M;
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
-                    const double2 k0 = __ldg(kd + t + r * T);
-                    const double2 k1 = __ldg(kd + M + t + r * T);
-                    cmac(O0[r], vv[r], k0);
-                    cmac(O1[r], vv[r], k1);
+                    cmac(O0[r], vv[r], kd[t + r * T]);
+                    cmac(O1[r], vv[r], kd[M + t + r * T]);
                 }
+                release(c);
             }
         }
-        fft_group<M, true>(O0, t, W, buf0, buf1, ex, gs);
-        fft_group<M, true>(O1, t, W, buf0, buf1, ex, gs);
+        fft_group<M, true>(O0, t, tw, buf0, buf1, ex, gs);
+        fft_group<M, true>(O1, t, tw, buf0, buf1, ex, gs);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             const int p = t + r * T;
-            const double2 uw = untw[p];
-            const double2 z0 = cmul(O0[r], uw);
-            const double2 z1 = cmul(O1[r], uw);
-            const long long r00 = round_half_away(z0.x), r01 = round_half_away(z0.y);
-            const long long r10 = round_half_away(z1.x), r11 = round_half_away(z1.y);
+            const double2 z0 = cmulc(O0[r], twist[r]);
+            const double2 z1 = cmulc(O1[r], twist[r]);
+            const long long r00 = round_product(z0.x), r01 = round_product(z0.y);
+            const long long r10 = round_product(z1.x), r11 = round_product(z1.y);
             if constexpr (TRACK_MARGIN) {
                 err_max = fmax(err_max, fabs(z0.x - (double)r00));
                 err_max = fmax(err_max, fabs(z0.y - (double)r01));
@@ -215,7 +273,8 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
 }
 
 // Fourier transform of the bootstrapping key rows (BootstrapKey.__init__,
-// bootstrap.py:319-323): centred residues -> fold, twist, forward DFT.
+// bootstrap.py:319-323): centred residues -> fold, twist, forward DFT, then
+// scaled by 1/M (exact) for the untwist-free epilogue above.
 // One group of T threads per polynomial; G polys per CTA.
 template <int M, int G>
 __global__ void __launch_bounds__(G * (M / 8))
@@ -224,17 +283,14 @@ bsk_forward_kernel(const int64_t* __restrict__ rows, int64_t npoly, int log2q,
     constexpr int T = M / 8;
     constexpr int PADM = PbsShape<M>::PADM;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2* W = reinterpret_cast<double2*>(smem_raw);
-    double2* twist = W + M;
-    double2* bufs = twist + 2 * M;  // skip untw
-    for (int k = threadIdx.x; k < 3 * M; k += blockDim.x) W[k] = tables[k];
-    __syncthreads();
     const int g = threadIdx.x / T, t = threadIdx.x % T;
     const int64_t poly = (int64_t)blockIdx.x * G + g;
     if (poly >= npoly) return;
-    double2* buf0 = bufs + g * 2 * PADM;
+    double2* buf0 = reinterpret_cast<double2*>(smem_raw) + g * 2 * PADM;
     double2* buf1 = buf0 + PADM;
     const GroupSync gs{1 + g, T};
+    Twiddles<M> tw;
+    load_twiddles<M>(tw, t, tables + M);
     const int64_t* src = rows + poly * 2 * M;
     const int64_t qm = (1ll << log2q) - 1;
     double2 vv[8];
@@ -243,12 +299,14 @@ bsk_forward_kernel(const int64_t* __restrict__ rows, int64_t npoly, int log2q,
         const int p = t + r * T;
         const int32_t lo = center_q((uint32_t)(src[p] & qm), log2q);
         const int32_t hi = center_q((uint32_t)(src[p + M] & qm), log2q);
-        vv[r] = cmul(make_double2((double)lo, (double)hi), twist[p]);
+        vv[r] = cmul(make_double2((double)lo, (double)hi), __ldg(tables + p));
     }
     int ex = 0;
-    fft_group<M, false>(vv, t, W, buf0, buf1, ex, gs);
+    fft_group<M, false>(vv, t, tw, buf0, buf1, ex, gs);
+    const double inv_m = 1.0 / M;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) out[poly * M + t + r * T] = vv[r];
+    for (int r = 0; r < 8; ++r)
+        out[poly * M + t + r * T] = make_double2(vv[r].x * inv_m, vv[r].y * inv_m);
 }
 
 }  // namespace fdsnn
