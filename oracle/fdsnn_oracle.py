@@ -298,3 +298,114 @@ def lwe_decrypt(A, b, s, q, p):
     m = div_round_half_away(phase * p, q) % p
     half = p // 2
     return ((m + half - 1) % p) - (half - 1)
+
+
+# ------------------------------------------------- compiled CPU baseline path
+# The reference accelerates the two elementwise stages of its CMux step with
+# numba (bootstrap.py:386-442).  The CPU-baseline leg of bench.py times the
+# same algorithm with the same library stack, so this module provides numba
+# versions of those two stages (written for this oracle); `blind_rotate_fast`
+# is checked bit-exact against `blind_rotate` in tests/test_oracle_pin.py.
+
+try:  # pragma: no cover - optional
+    import numba as _nb
+except Exception:  # pragma: no cover
+    _nb = None
+
+if _nb is not None:
+
+    @_nb.njit(cache=True)
+    def _digits_twisted(acc, k, twist, out, q, base, levels):
+        # powers of two throughout: reductions are masks, digit division a shift
+        B, _, N = acc.shape
+        M = N // 2
+        qm, half_q, m2n = q - 1, q // 2, 2 * N - 1
+        bm, hb = base - 1, base // 2 - 1
+        shift = 0
+        while (1 << shift) < base:
+            shift += 1
+        for bi in range(B):
+            kk = k[bi]
+            for c in range(2):
+                a = acc[bi, c]
+                for j in range(M):
+                    s0 = (j - kk) & m2n
+                    v0 = -a[s0 - N] if s0 >= N else a[s0]
+                    x0 = (v0 - a[j]) & qm
+                    if x0 >= half_q:
+                        x0 -= q
+                    s1 = (j + M - kk) & m2n
+                    v1 = -a[s1 - N] if s1 >= N else a[s1]
+                    x1 = (v1 - a[j + M]) & qm
+                    if x1 >= half_q:
+                        x1 -= q
+                    tw = twist[j]
+                    for lv in range(levels):
+                        d0 = ((x0 + hb) & bm) - hb
+                        d1 = ((x1 + hb) & bm) - hb
+                        x0 = (x0 - d0) >> shift
+                        x1 = (x1 - d1) >> shift
+                        out[bi, c * levels + lv, j] = complex(d0, d1) * tw
+
+    @_nb.njit(cache=True)
+    def _round_add(acc, y, untw, q):
+        B, _, N = acc.shape
+        M = N // 2
+        qm = q - 1
+        for bi in range(B):
+            for c in range(2):
+                for j in range(M):
+                    z = y[bi, c, j] * untw[j]
+                    r0 = np.floor(z.real + 0.5) if z.real >= 0 else np.ceil(z.real - 0.5)
+                    r1 = np.floor(z.imag + 0.5) if z.imag >= 0 else np.ceil(z.imag - 0.5)
+                    acc[bi, c, j] = (acc[bi, c, j] + np.int64(r0)) & qm
+                    acc[bi, c, j + M] = (acc[bi, c, j + M] + np.int64(r1)) & qm
+
+
+def blind_rotate_fast(acc, a2N, key: OracleKey):
+    """Same CMux chain as `blind_rotate`, numba-compiled digit/round stages."""
+    if _nb is None:
+        return blind_rotate(acc, a2N, key)
+    prm = key.prm
+    q, N, Bg, l = prm["q"], prm["N"], prm["Bg"], prm["l"]
+    M = N // 2
+    acc = np.array(acc, dtype=np.int64)
+    B = acc.shape[0]
+    dig = np.empty((B, 2 * l, M), dtype=np.complex128)
+    untw = key.tr.untwist / M
+    for i in range(a2N.shape[1]):
+        k = np.ascontiguousarray(a2N[:, i], dtype=np.int64)
+        if not k.any():
+            continue
+        _digits_twisted(acc, k, key.tr.twist, dig, q, Bg, l)
+        dig_f = np.fft.ifft(dig, axis=-1, norm="forward")
+        prod = np.einsum("bdm,dom->bom", dig_f, key.ek_f[i])
+        _round_add(acc, np.fft.fft(prod, axis=-1), untw, q)
+    return acc
+
+
+def key_switch_fast(ea, eb, key: OracleKey):
+    """`key_switch` as float64 BLAS products, exact below 2^52 like the
+    reference's own assertion (bootstrap.py:504-508)."""
+    prm = key.prm
+    q = prm["q"]
+    if not hasattr(key, "_ksk_Af"):
+        key._ksk_Af = key.ksk_A.astype(np.float64)
+        key._ksk_bf = key.ksk_b.astype(np.float64)
+    dig = gadget_decompose(ea, q, prm["ks_base"], prm["ks_l"])
+    flat = np.swapaxes(dig, -2, -1).reshape(ea.shape[0], -1).astype(np.float64)
+    out_a = (-(flat @ key._ksk_Af)).astype(np.int64) % q
+    out_b = (np.asarray(eb, dtype=np.int64) - (flat @ key._ksk_bf).astype(np.int64)) % q
+    return out_a, out_b
+
+
+def lif_step_fast(vA, vb, iA, ib, v_th_hat, leak_num, leak_den, key: OracleKey):
+    """`lif_step` with the compiled blind rotation and BLAS key switch (CPU
+    baseline leg of bench.py; bit-exact with `lif_step`)."""
+    global blind_rotate, key_switch
+    saved = blind_rotate, key_switch
+    try:
+        blind_rotate, key_switch = blind_rotate_fast, key_switch_fast  # looked up at call time
+        return lif_step(vA, vb, iA, ib, v_th_hat, leak_num, leak_den, key)
+    finally:
+        blind_rotate, key_switch = saved

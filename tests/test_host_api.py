@@ -1,0 +1,167 @@
+"""Host-side mirror of the reference API (CPU only): key generation parity,
+parameter validation, LUTs, encryption, network lowering, error types."""
+import hashlib
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, make_keys
+from paper_2309_09025_b200 import bootstrap, errors, lwe, network, neuron, params, rgsw, ring
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(np.asarray(a, dtype=np.int64)).tobytes())
+    return h.hexdigest()
+
+
+def test_key_generation_matches_reference_digests(toy, toy64, desk, c4prm):
+    """Keys from a seed are bit-identical to the reference's (keys.json written by
+    running the reference's gen_bootstrap_key)."""
+    path = os.path.join(GOLDEN, "keys.json")
+    want = json.load(open(path))
+    for name, prm in (("toy", toy), ("toy64", toy64), ("desk1024", desk), ("c4", c4prm)):
+        w = want[name]
+        sk, zk, bsk = make_keys(prm, w["seed"])
+        assert sha(sk.s) == w["sk"] and sha(zk.z) == w["zk"]
+        assert sha(bsk.rows) == w["rows"]
+        assert sha(bsk.ksk.A) == w["ksk_A"] and sha(bsk.ksk.b) == w["ksk_b"]
+        assert prm.digest() == w["params_digest"]
+
+
+def test_params_validation():
+    with pytest.raises(errors.ParameterError):
+        params.FheParams(n=8, q=1000, N=512, p=8, sigma=1, gadget=params.GadgetParams(64, 2),
+                         ks_base=8, ks_levels=4, sigma_bk=0.1, sigma_ks=0.1)
+    with pytest.raises(errors.ParameterError):  # gadget must cover q
+        params.FheParams(n=8, q=1 << 25, N=1024, p=8, sigma=1, gadget=params.GadgetParams(1 << 7, 3),
+                         ks_base=4, ks_levels=8, sigma_bk=0.1, sigma_ks=0.1)
+    with pytest.raises(errors.ParameterError):
+        params.preset("TOY").with_p(12)
+    with pytest.raises(errors.ConfigurationError):
+        params.preset("nope")
+    d = params.preset("DESK")
+    assert (d.grid, d.delta, d.noise_bound) == (1 << 14, 1 << 14, 1 << 13)
+    assert params.FheParams.from_dict(d.to_dict()) == d
+
+
+def test_program_functions():
+    g = neuron.g_fire(8)
+    assert all(g(m) == 1 for m in range(4)) and all(g(m) == -1 for m in range(-4, 0))
+    with pytest.raises((errors.DomainError, errors.ParameterError)):
+        bootstrap.ProgramFunction([1] * 8, 8)
+    lif = neuron.LifParams(tau=2, theta=10)
+    gr = neuron.g_reset(lif, 1024)
+    assert (gr(0), gr(5), gr(19), gr(20), gr(-3)) == (0, 3, 10, 0, 0)
+    with pytest.raises(errors.ParameterError):
+        neuron.g_reset(neuron.LifParams(tau=2, theta=100), 64)
+    rng = np.random.default_rng(0)
+    for p in (8, 64, 1024):
+        g = bootstrap.make_program(dict(enumerate(rng.integers(-p // 2 + 1, p // 2 + 1, p // 2))), p)
+        for v in range(p // 2):
+            assert (g(v - p // 2) + g(v)) % p == 0
+
+
+def test_test_polynomial_and_accumulator(toy):
+    g = neuron.g_fire(toy.p)
+    v = bootstrap.test_polynomial(g, toy)
+    want = np.array([(toy.delta * g((i * toy.p) // (2 * toy.N))) % toy.q for i in range(toy.N)])
+    assert np.array_equal(v, want)
+    acc = bootstrap.initialize_accumulator(g, 0, toy)
+    assert np.array_equal(acc.b, want) and not np.any(acc.a)
+    z = bootstrap.make_program(lambda m: 0, toy.p)
+    for b2N in (0, 17, 511, 1023):
+        a = bootstrap.initialize_accumulator(z, b2N, toy)
+        assert not np.any(a.a) and not np.any(a.b)
+
+
+def test_lif_params_and_plain_steps():
+    lif = neuron.LifParams(tau=2, theta=10)
+    assert lif.v_th_hat == 20 and (lif.leak_num, lif.leak_den) == (1, 2)
+    assert neuron.LifParams(tau=math.inf, theta=10).v_th_hat == 10
+    assert (neuron.LifParams(tau=2, theta=10, leak_convention="theta").leak_num) == 9
+    with pytest.raises(errors.ParameterError):
+        neuron.LifParams(tau=1, theta=10)
+    s, nxt = neuron.plain_lif_step(neuron.PlainLifState(0), 25, lif)
+    assert (s, nxt.v_hat) == (2, 0)
+    s, nxt = neuron.plain_lif_step(neuron.PlainLifState(0), 10, lif)
+    assert (s, nxt.v_hat) == (0, 5)
+    with pytest.raises(errors.OverflowViolation):
+        neuron.plain_lif_step(neuron.PlainLifState(0), 600, lif, p=1024)
+
+
+def test_encrypt_decrypt_roundtrip(toy64, toy64_keys):
+    sk, _, _ = toy64_keys
+    rng = np.random.default_rng(3)
+    ms = rng.integers(-31, 33, 500)
+    A, b = lwe.encrypt_batch(ms, sk, toy64, rng)
+    assert np.array_equal(lwe.decrypt_batch(A, b, sk, toy64), ms)
+    assert np.all(A % toy64.grid == 0)
+    with pytest.raises(errors.DomainError):
+        lwe.encrypt_batch(np.array([-32]), sk, toy64, rng)
+    ct = lwe.weight_sum([lwe.encrypt(1, sk, toy64, rng), lwe.encrypt(2, sk, toy64, rng)], [3, -1])
+    assert lwe.decrypt(ct, sk, toy64) == 1
+
+
+def test_gadget_host_rule(desk):
+    rng = np.random.default_rng(5)
+    x = rng.integers(0, desk.q, (3, 16))
+    d = rgsw.gadget_decompose(x, desk.q, desk.gadget)
+    assert np.array_equal(rgsw.gadget_recompose(d, desk.gadget) % desk.q, x)
+    assert list(rgsw.gadget_decompose(np.array([2048]), 1 << 12, params.GadgetParams(16, 3)).ravel()) == [0, 0, 8]
+
+
+def test_ring_helpers():
+    assert ring.rescale(4095, 4096, 1024) == 0
+    assert ring.round_half_away(0.5) == 1 and ring.round_half_away(-0.5) == -1
+    a = np.random.default_rng(1).integers(-100, 100, 64)
+    z = np.random.default_rng(2).integers(0, 2, 64)
+    full = np.convolve(a, z)
+    want = (full[:64] - np.concatenate([full[64:], [0]])) % 4096
+    assert np.array_equal(ring.negacyclic_mul_raw(a, z, 4096), want)
+
+
+def test_conv_and_pool_lowering():
+    rng = np.random.default_rng(6)
+    w = rng.integers(-3, 4, (2, 1, 3, 3))
+    m, shape = network.conv_matrix(w, (1, 5, 6), (2, 1), (1, 0))
+    x = rng.integers(0, 5, (1, 5, 6))
+    # naive conv
+    oh, ow = shape[1], shape[2]
+    xp = np.pad(x, ((0, 0), (1, 1), (0, 0)))
+    want = np.zeros(shape, np.int64)
+    for o in range(2):
+        for y in range(oh):
+            for xx in range(ow):
+                want[o, y, xx] = (w[o, 0] * xp[0, 2 * y:2 * y + 3, xx:xx + 3]).sum()
+    assert shape == (2, 3, 4) and np.array_equal(m @ x.ravel(), want.ravel())
+    pm, ps = network.pool_matrix((2, 4, 4), (2, 2))
+    assert ps == (2, 2, 2) and np.all(pm.sum(axis=1) == 4) and np.all(pm.sum(axis=0) == 1)
+
+
+def test_discretize_scale_rules():
+    lin = network.CsnnModel(
+        arch=({"type": "linear", "out_features": 4}, {"type": "spiking"},
+              {"type": "linear", "out_features": 2}, {"type": "spiking"}),
+        weights=(np.full((4, 4), 0.5), np.full((2, 4), 0.126)), input_shape=(1, 2, 2), T=1, L=1, tau=None)
+    net = network.discretize(lin, 40)
+    second = [l for l in net.layers if isinstance(l, network.WeightLayer)][1]
+    assert second.scale == 20 and np.all(second.matrix == 3)
+    assert net.bootstrap_count() == 2 * (4 + 2)
+    doc = lin.to_dict()
+    again = network.CsnnModel.from_dict(doc)
+    assert again.T == 1 and np.array_equal(again.weights[1], lin.weights[1])
+    doc["format"] = "fdsnn-model/999"
+    with pytest.raises(errors.SerializationError):
+        network.CsnnModel.from_dict(doc)
+
+
+def test_ciphertext_tensor_checks(toy):
+    with pytest.raises(errors.ParameterError):
+        network.CiphertextTensor((3,), np.zeros((2, toy.n)), np.zeros(2), toy.q)
+    z = network.zero_states(5, toy)
+    assert z.count == 5 and not np.any(z.A)
