@@ -148,22 +148,60 @@ FDSNN_DEV void load_twiddles(Twiddles<M>& tw, int t, const double2* __restrict__
     load_twiddles_pass<M, 1>(tw, t, tab);
 }
 
+
+// Twiddle providers: fetch<PASS>(w) fills w[r-1] = e^{2 pi i r jm/(NS R)},
+// r = 1..R-1, for this thread's interior pass PASS.
+template <int M>
+struct TwiddlesInRegs {
+    Twiddles<M> tw;
+    template <int PASS>
+    FDSNN_DEV void fetch(double2 (&w)[8]) const {
+#pragma unroll
+        for (int r = 0; r < 7; ++r) w[r] = tw.w[PASS][r];
+    }
+};
+
+// Tensor-memory resident twiddles: pass p occupies columns (p-1)*32..+31 of
+// the thread's TMEM lane (8 complex, entries r-1 = 0..6), so the register file
+// only holds the current pass's factors.
+template <int M>
+struct TwiddlesInTmem {
+    uint32_t base;
+    template <int PASS>
+    FDSNN_DEV void fetch(double2 (&w)[8]) const {
+        double2 a[4];
+        tmem_ld4c(base + (PASS - 1) * 32, a);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) w[r] = a[r];
+        if constexpr (PassInfo<M, PASS>::R > 5) {
+            tmem_ld4c(base + (PASS - 1) * 32 + 16, a);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) w[4 + r] = a[r];
+        }
+    }
+};
+
 // One Stockham pass.  v holds 8/R independent R-point groups.
 template <int M, int PASS, bool INV>
-FDSNN_DEV void pass_body(double2 (&v)[8], const Twiddles<M>& tw) {
+FDSNN_DEV void pass_body(double2 (&v)[8], const double2 (&w)[8]) {
     constexpr int R = PassInfo<M, PASS>::R;
     constexpr int NS = PassInfo<M, PASS>::NS;
 #pragma unroll
     for (int s = 0; s < 8 / R; ++s) {
         if constexpr (NS > 1) {
 #pragma unroll
-            for (int r = 1; r < R; ++r) {
-                const double2 w = tw.w[PASS][r - 1];
-                v[s * R + r] = INV ? cmulc(v[s * R + r], w) : cmul(v[s * R + r], w);
-            }
+            for (int r = 1; r < R; ++r)
+                v[s * R + r] = INV ? cmulc(v[s * R + r], w[r - 1]) : cmul(v[s * R + r], w[r - 1]);
         }
         dftR<R, INV>(&v[s * R]);
     }
+}
+
+template <int M, int PASS, bool INV, class TW>
+FDSNN_DEV void pass_tw(double2 (&v)[8], const TW& tw) {
+    double2 w[8];
+    if constexpr (PASS > 0) tw.template fetch<PASS>(w);
+    pass_body<M, PASS, INV>(v, w);
 }
 
 template <int M, int PASS>
@@ -195,12 +233,12 @@ FDSNN_DEV void pass_load(double2 (&v)[8], int t, const double2* __restrict__ buf
 // Full transform: v (points t + rT) -> v (frequencies t + rT).
 // `ex` is the running exchange parity (alternates the two exchange buffers so
 // that a single barrier per exchange is race free across consecutive FFTs).
-template <int M, bool INV>
-FDSNN_DEV void fft_group(double2 (&v)[8], int t, const Twiddles<M>& tw,
+template <int M, bool INV, class TW>
+FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
                          double2* __restrict__ buf0, double2* __restrict__ buf1,
                          int& ex, const GroupSync& gs) {
     constexpr int P = Schedule<M>::P;
-    pass_body<M, 0, INV>(v, tw);
+    pass_tw<M, 0, INV>(v, tw);
 #define FDSNN_FFT_STEP(PS)                                        \
     if constexpr (PS < P) {                                       \
         double2* b = ex ? buf1 : buf0;                            \
@@ -208,12 +246,45 @@ FDSNN_DEV void fft_group(double2 (&v)[8], int t, const Twiddles<M>& tw,
         gs.sync();                                                \
         pass_load<M, PS>(v, t, b);                                \
         ex ^= 1;                                                  \
-        pass_body<M, PS, INV>(v, tw);                             \
+        pass_tw<M, PS, INV>(v, tw);                               \
     }
     FDSNN_FFT_STEP(1)
     FDSNN_FFT_STEP(2)
     FDSNN_FFT_STEP(3)
 #undef FDSNN_FFT_STEP
+}
+
+// Two independent transforms interleaved (double ILP, shared barriers): v0
+// exchanges through buf0, v1 through buf1.  Each exchange is fenced on both
+// sides (write-after-read on the buffers), so it is safe whatever the buffers
+// were last used for.
+template <int M, bool INV, class TW>
+FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& tw,
+                          double2* __restrict__ buf0, double2* __restrict__ buf1,
+                          const GroupSync& gs) {
+    constexpr int P = Schedule<M>::P;
+    {
+        double2 w[8];
+        pass_body<M, 0, INV>(v0, w);
+        pass_body<M, 0, INV>(v1, w);
+    }
+#define FDSNN_FFT2_STEP(PS)                                       \
+    if constexpr (PS < P) {                                       \
+        gs.sync();                                                \
+        pass_store<M, PS - 1>(v0, t, buf0);                       \
+        pass_store<M, PS - 1>(v1, t, buf1);                       \
+        gs.sync();                                                \
+        pass_load<M, PS>(v0, t, buf0);                            \
+        pass_load<M, PS>(v1, t, buf1);                            \
+        double2 w[8];                                             \
+        tw.template fetch<PS>(w);                                 \
+        pass_body<M, PS, INV>(v0, w);                             \
+        pass_body<M, PS, INV>(v1, w);                             \
+    }
+    FDSNN_FFT2_STEP(1)
+    FDSNN_FFT2_STEP(2)
+    FDSNN_FFT2_STEP(3)
+#undef FDSNN_FFT2_STEP
 }
 
 }  // namespace fdsnn

@@ -79,6 +79,24 @@ FDSNN_DEV void load_twist(double2 (&tw)[8], int t, const double2* __restrict__ t
     for (int r = 0; r < 8; ++r) tw[r] = __ldg(tables + t + r * (M / 8));
 }
 
+// TMEM layout per lane (128 columns): interior-pass twiddles of pass p at
+// columns (p-1)*32 (8 complex), twist factors at 96 (8 complex).  The two warps
+// sharing a TMEM lane quadrant (w and w+4) always have the same in-group
+// thread index t, hence identical constants, so one copy per lane suffices.
+constexpr uint32_t PBS_TMEM_COLS = 128;
+constexpr uint32_t PBS_TMEM_TWIST = 96;
+
+template <int M>
+FDSNN_DEV void tmem_twist(uint32_t lane_base, double2 (&tw)[8]) {
+    double2 a[4];
+    tmem_ld4c(lane_base + PBS_TMEM_TWIST, a);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) tw[r] = a[r];
+    tmem_ld4c(lane_base + PBS_TMEM_TWIST + 16, a);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) tw[4 + r] = a[r];
+}
+
 template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN>
 __global__ void __launch_bounds__(PBS_THREADS, 1)
 pbs_blind_rotate_kernel(const PbsArgs args) {
@@ -97,7 +115,9 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     uint64_t* empty = full + S;
+    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem_raw + 96);
     double2* ring = reinterpret_cast<double2*>(smem_raw + 128);
+    const int warp = threadIdx.x / 32;
     const int g = threadIdx.x / T;
     const int t = threadIdx.x % T;
     unsigned char* mine = smem_raw + 128 + S * CHUNK + g * pbs_group_bytes<M>(N, n);
@@ -109,6 +129,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     const int64_t V = (int64_t)args.nlut * args.count;
     const int64_t v0 = (int64_t)blockIdx.x * G;
     const int nact = (int)((V - v0) < G ? (V - v0) : G);  // active groups in this CTA
+    const bool active = g < nact;
     const int64_t nchunks = (int64_t)n * 2 * L;
     const bool producer = threadIdx.x == 0;
     if (producer) {
@@ -118,21 +139,61 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
         }
         fence_mbar_init();
     }
+    if (warp == 0) tmem_alloc(tmem_base_slot, PBS_TMEM_COLS);
+    // per-thread constants -> TMEM (lanes of warps 0-3 cover all quadrants)
+    if (warp < 4 && active) {
+        TwiddlesInRegs<M> twr;
+        load_twiddles<M>(twr.tw, t, args.tables + M);
+        double2 twist[8];
+        load_twist<M>(twist, t, args.tables);
+        tmem_fence_after();
+        __syncwarp();
+    }
+    tmem_fence_before();
     __syncthreads();
+    tmem_fence_after();
+    const uint32_t lane_base = *tmem_base_slot + ((uint32_t)((warp % 4) * 32) << 16);
+    if (warp < 4 && active) {
+        TwiddlesInRegs<M> twr;
+        load_twiddles<M>(twr.tw, t, args.tables + M);
+#pragma unroll
+        for (int p = 1; p < Schedule<M>::P; ++p) {
+            double d[8];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    d[2 * r] = twr.tw.w[p][4 * h + r < 7 ? 4 * h + r : 6].x;
+                    d[2 * r + 1] = twr.tw.w[p][4 * h + r < 7 ? 4 * h + r : 6].y;
+                }
+                tmem_st16(lane_base + (p - 1) * 32 + 16 * h, d);
+            }
+        }
+        double2 twist[8];
+        load_twist<M>(twist, t, args.tables);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double d[8];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) { d[2 * r] = twist[4 * h + r].x; d[2 * r + 1] = twist[4 * h + r].y; }
+            tmem_st16(lane_base + PBS_TMEM_TWIST + 16 * h, d);
+        }
+        tmem_wait_st();
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
     if (producer) {
         for (int s = 0; s < S && s < nchunks; ++s) {
             mbar_arrive_expect_tx(&full[s], CHUNK);
             bulk_g2s(ring + (size_t)s * 2 * M, args.bsk + (size_t)s * 2 * M, CHUNK, &full[s]);
         }
     }
-    if (g >= nact) return;  // only group barriers / mbarriers are used below
+
+    if (active) {
     const int64_t v = v0 + g;
     const GroupSync gs{1 + g, T};
-
-    Twiddles<M> tw;
-    load_twiddles<M>(tw, t, args.tables + M);
-    double2 twist[8];
-    load_twist<M>(twist, t, args.tables);
+    const TwiddlesInTmem<M> tw{lane_base};
 
     // ---------------- setup: modulus switch + accumulator init -------------
     if constexpr (!MODE_RAW) {
@@ -212,13 +273,17 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
             }
             for (int lvl = 0; lvl < L; ++lvl, ++c) {
                 double2 vv[8];
+                {
+                    double2 twist[8];
+                    tmem_twist<M>(lane_base, twist);
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const int32_t d1 = ((xlo[r] + halfB1) & bmask) - halfB1;
-                    const int32_t d2 = ((xhi[r] + halfB1) & bmask) - halfB1;
-                    xlo[r] = (xlo[r] - d1) >> bg;
-                    xhi[r] = (xhi[r] - d2) >> bg;
-                    vv[r] = cmul(make_double2((double)d1, (double)d2), twist[r]);
+                    for (int r = 0; r < 8; ++r) {
+                        const int32_t d1 = ((xlo[r] + halfB1) & bmask) - halfB1;
+                        const int32_t d2 = ((xhi[r] + halfB1) & bmask) - halfB1;
+                        xlo[r] = (xlo[r] - d1) >> bg;
+                        xhi[r] = (xhi[r] - d2) >> bg;
+                        vv[r] = cmul(make_double2((double)d1, (double)d2), twist[r]);
+                    }
                 }
                 fft_group<M, false>(vv, t, tw, buf0, buf1, ex, gs);
                 const int s = (int)(c % S);
@@ -232,25 +297,28 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                 release(c);
             }
         }
-        fft_group<M, true>(O0, t, tw, buf0, buf1, ex, gs);
-        fft_group<M, true>(O1, t, tw, buf0, buf1, ex, gs);
+        fft_group2<M, true>(O0, O1, t, tw, buf0, buf1, gs);
+        {
+            double2 twist[8];
+            tmem_twist<M>(lane_base, twist);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int p = t + r * T;
-            const double2 z0 = cmulc(O0[r], twist[r]);
-            const double2 z1 = cmulc(O1[r], twist[r]);
-            const long long r00 = round_product(z0.x), r01 = round_product(z0.y);
-            const long long r10 = round_product(z1.x), r11 = round_product(z1.y);
-            if constexpr (TRACK_MARGIN) {
-                err_max = fmax(err_max, fabs(z0.x - (double)r00));
-                err_max = fmax(err_max, fabs(z0.y - (double)r01));
-                err_max = fmax(err_max, fabs(z1.x - (double)r10));
-                err_max = fmax(err_max, fabs(z1.y - (double)r11));
+            for (int r = 0; r < 8; ++r) {
+                const int p = t + r * T;
+                const double2 z0 = cmulc(O0[r], twist[r]);
+                const double2 z1 = cmulc(O1[r], twist[r]);
+                const long long r00 = round_product(z0.x), r01 = round_product(z0.y);
+                const long long r10 = round_product(z1.x), r11 = round_product(z1.y);
+                if constexpr (TRACK_MARGIN) {
+                    err_max = fmax(err_max, fabs(z0.x - (double)r00));
+                    err_max = fmax(err_max, fabs(z0.y - (double)r01));
+                    err_max = fmax(err_max, fabs(z1.x - (double)r10));
+                    err_max = fmax(err_max, fabs(z1.y - (double)r11));
+                }
+                acc[p] = (int32_t)(((uint32_t)acc[p] + (uint32_t)r00) & qmask);
+                acc[p + M] = (int32_t)(((uint32_t)acc[p + M] + (uint32_t)r01) & qmask);
+                acc[N + p] = (int32_t)(((uint32_t)acc[N + p] + (uint32_t)r10) & qmask);
+                acc[N + p + M] = (int32_t)(((uint32_t)acc[N + p + M] + (uint32_t)r11) & qmask);
             }
-            acc[p] = (int32_t)(((uint32_t)acc[p] + (uint32_t)r00) & qmask);
-            acc[p + M] = (int32_t)(((uint32_t)acc[p + M] + (uint32_t)r01) & qmask);
-            acc[N + p] = (int32_t)(((uint32_t)acc[N + p] + (uint32_t)r10) & qmask);
-            acc[N + p + M] = (int32_t)(((uint32_t)acc[N + p + M] + (uint32_t)r11) & qmask);
         }
         gs.sync();
     }
@@ -269,6 +337,13 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
             out[j] = a;
         }
         if (t == 0) out[N] = (uint32_t)acc[N];
+    }
+    }  // active
+    tmem_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tmem_fence_after();
+        tmem_dealloc(*tmem_base_slot, PBS_TMEM_COLS);
     }
 }
 
@@ -289,8 +364,8 @@ bsk_forward_kernel(const int64_t* __restrict__ rows, int64_t npoly, int log2q,
     double2* buf0 = reinterpret_cast<double2*>(smem_raw) + g * 2 * PADM;
     double2* buf1 = buf0 + PADM;
     const GroupSync gs{1 + g, T};
-    Twiddles<M> tw;
-    load_twiddles<M>(tw, t, tables + M);
+    TwiddlesInRegs<M> tw;
+    load_twiddles<M>(tw.tw, t, tables + M);
     const int64_t* src = rows + poly * 2 * M;
     const int64_t qm = (1ll << log2q) - 1;
     double2 vv[8];
