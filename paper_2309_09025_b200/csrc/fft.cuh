@@ -149,35 +149,34 @@ FDSNN_DEV void load_twiddles(Twiddles<M>& tw, int t, const double2* __restrict__
 }
 
 
-// Twiddle providers: fetch<PASS>(w) fills w[r-1] = e^{2 pi i r jm/(NS R)},
-// r = 1..R-1, for this thread's interior pass PASS.
+// Twiddle providers.  issue<PASS>(raw) starts fetching the R-1 factors
+// e^{2 pi i r jm/(NS R)} of this thread's interior pass PASS; finish<PASS>
+// (raw, w) completes the fetch into w[r-1].  The FFT issues the fetch before
+// the pass's shared-memory exchange so its latency hides behind the barrier.
 template <int M>
 struct TwiddlesInRegs {
     Twiddles<M> tw;
     template <int PASS>
-    FDSNN_DEV void fetch(double2 (&w)[8]) const {
+    FDSNN_DEV void issue(uint32_t (&)[32]) const {}
+    template <int PASS>
+    FDSNN_DEV void finish(uint32_t (&)[32], double2 (&w)[8]) const {
 #pragma unroll
         for (int r = 0; r < 7; ++r) w[r] = tw.w[PASS][r];
     }
 };
 
 // Tensor-memory resident twiddles: pass p occupies columns (p-1)*32..+31 of
-// the thread's TMEM lane (8 complex, entries r-1 = 0..6), so the register file
-// only holds the current pass's factors.
+// the thread's TMEM lane (8 complex, entries r-1 = 0..6).
 template <int M>
 struct TwiddlesInTmem {
     uint32_t base;
     template <int PASS>
-    FDSNN_DEV void fetch(double2 (&w)[8]) const {
-        double2 a[4];
-        tmem_ld4c(base + (PASS - 1) * 32, a);
+    FDSNN_DEV void issue(uint32_t (&raw)[32]) const { tmem_ld32_async(base + (PASS - 1) * 32, raw); }
+    template <int PASS>
+    FDSNN_DEV void finish(uint32_t (&raw)[32], double2 (&w)[8]) const {
+        tmem_wait32(raw);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) w[r] = a[r];
-        if constexpr (PassInfo<M, PASS>::R > 5) {
-            tmem_ld4c(base + (PASS - 1) * 32 + 16, a);
-#pragma unroll
-            for (int r = 0; r < 4; ++r) w[4 + r] = a[r];
-        }
+        for (int r = 0; r < 7; ++r) w[r] = words_c(raw, r);
     }
 };
 
@@ -195,13 +194,6 @@ FDSNN_DEV void pass_body(double2 (&v)[8], const double2 (&w)[8]) {
         }
         dftR<R, INV>(&v[s * R]);
     }
-}
-
-template <int M, int PASS, bool INV, class TW>
-FDSNN_DEV void pass_tw(double2 (&v)[8], const TW& tw) {
-    double2 w[8];
-    if constexpr (PASS > 0) tw.template fetch<PASS>(w);
-    pass_body<M, PASS, INV>(v, w);
 }
 
 template <int M, int PASS>
@@ -230,23 +222,38 @@ FDSNN_DEV void pass_load(double2 (&v)[8], int t, const double2* __restrict__ buf
     }
 }
 
+struct NoHook {
+    FDSNN_DEV void operator()() const {}
+};
+
 // Full transform: v (points t + rT) -> v (frequencies t + rT).
 // `ex` is the running exchange parity (alternates the two exchange buffers so
 // that a single barrier per exchange is race free across consecutive FFTs).
-template <int M, bool INV, class TW>
+// `pre_last` runs after the last exchange and twiddle fetch, before the last
+// pass's arithmetic
+// (used to start the key fetch of the following MAC).
+template <int M, bool INV, class TW, class HOOK = NoHook>
 FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
                          double2* __restrict__ buf0, double2* __restrict__ buf1,
-                         int& ex, const GroupSync& gs) {
+                         int& ex, const GroupSync& gs, const HOOK& pre_last = HOOK()) {
     constexpr int P = Schedule<M>::P;
-    pass_tw<M, 0, INV>(v, tw);
+    {
+        double2 w[8];
+        pass_body<M, 0, INV>(v, w);
+    }
 #define FDSNN_FFT_STEP(PS)                                        \
     if constexpr (PS < P) {                                       \
+        uint32_t raw[32];                                         \
+        tw.template issue<PS>(raw);                               \
         double2* b = ex ? buf1 : buf0;                            \
         pass_store<M, PS - 1>(v, t, b);                           \
         gs.sync();                                                \
         pass_load<M, PS>(v, t, b);                                \
         ex ^= 1;                                                  \
-        pass_tw<M, PS, INV>(v, tw);                               \
+        double2 w[8];                                             \
+        tw.template finish<PS>(raw, w);                           \
+        if constexpr (PS == P - 1) pre_last();                    \
+        pass_body<M, PS, INV>(v, w);                              \
     }
     FDSNN_FFT_STEP(1)
     FDSNN_FFT_STEP(2)
@@ -258,10 +265,10 @@ FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
 // exchanges through buf0, v1 through buf1.  Each exchange is fenced on both
 // sides (write-after-read on the buffers), so it is safe whatever the buffers
 // were last used for.
-template <int M, bool INV, class TW>
+template <int M, bool INV, class TW, class HOOK = NoHook>
 FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& tw,
                           double2* __restrict__ buf0, double2* __restrict__ buf1,
-                          const GroupSync& gs) {
+                          const GroupSync& gs, const HOOK& pre_last = HOOK()) {
     constexpr int P = Schedule<M>::P;
     {
         double2 w[8];
@@ -270,6 +277,8 @@ FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& t
     }
 #define FDSNN_FFT2_STEP(PS)                                       \
     if constexpr (PS < P) {                                       \
+        uint32_t raw[32];                                         \
+        tw.template issue<PS>(raw);                               \
         gs.sync();                                                \
         pass_store<M, PS - 1>(v0, t, buf0);                       \
         pass_store<M, PS - 1>(v1, t, buf1);                       \
@@ -277,7 +286,8 @@ FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& t
         pass_load<M, PS>(v0, t, buf0);                            \
         pass_load<M, PS>(v1, t, buf1);                            \
         double2 w[8];                                             \
-        tw.template fetch<PS>(w);                                 \
+        tw.template finish<PS>(raw, w);                           \
+        if constexpr (PS == P - 1) pre_last();                    \
         pass_body<M, PS, INV>(v0, w);                             \
         pass_body<M, PS, INV>(v1, w);                             \
     }

@@ -10,16 +10,25 @@
 //   sample extract       bootstrap.py:484-488
 //
 // Work decomposition: one group of T = M/8 threads owns one accumulator
-// (2 x N int32 in shared memory) for all n CMux steps; G groups per CTA.
-// Per step and accumulator: 2L forward transforms of the signed gadget digits
-// of (X^k - 1)*ACC, a register-resident MAC against the Fourier-domain key
-// slice, 2 inverse transforms, round and add back.  The accumulator never
-// leaves shared memory until the final sample extraction.
+// (2 x N int32 in shared memory) for all n CMux steps; G = 256/T groups per
+// CTA.  Per step and accumulator: 2L forward transforms of the signed gadget
+// digits of (X^k - 1)*ACC, a register MAC against the Fourier-domain key
+// slice, 2 inverse transforms (interleaved), round and add back.
 //
-// Register-resident constants per thread: the twist e^{i pi p/N} of its 8
-// points and the interior-pass twiddles (fft.cuh Twiddles).  The device
-// Fourier key is pre-scaled by 1/M (exact: M is a power of two), so the
-// untwist of the inverse transform is a plain multiply by conj(twist).
+// Memory roles on sm_100a:
+//   * shared memory: accumulators, FFT exchange buffers, and a ring of S key
+//     chunks (one (step, digit) chunk = 2 polys x M complex) filled by the TMA
+//     engine (cp.async.bulk + mbarrier full/empty) and shared by the G
+//     accumulators of the CTA;
+//   * tensor memory (TMEM, per-thread lanes, tcgen05.ld): the thread's
+//     interior-pass twiddles and twist factors, fetched asynchronously ahead
+//     of use so they cost neither registers nor shared-memory bandwidth;
+//   * registers: the 8-point FFT vector and the 2 x 8 frequency accumulators.
+// (Streaming the key chunks into TMEM with tcgen05.cp was measured too: it
+// removes the key's shared-memory reads but the copy engine sustains only
+// ~18 B/clk/SM with warpx2 multicast and the pipeline ran 25% slower.)
+// The Fourier key is pre-scaled by 1/M (exact), so the inverse transform's
+// untwist is a multiply by conj(twist).
 #pragma once
 #include "fft.cuh"
 
@@ -59,10 +68,6 @@ __host__ __device__ constexpr size_t pbs_group_bytes(int N, int n) {
            + (((size_t)n * sizeof(uint16_t) + 15) & ~(size_t)15);  // a2N
 }
 
-// CTA = 256 threads = G groups of T = M/8; the key slice of each CMux step is
-// streamed through a ring of S stages by the TMA engine (cp.async.bulk), one
-// stage per (step, digit) chunk = 2 output polys x M complex = 32*M bytes,
-// shared by all G accumulators of the CTA.
 constexpr int PBS_THREADS = 256;
 template <int M> struct PbsRing { static constexpr int S = (M == 1024) ? 3 : 4; };
 template <int M>
@@ -79,23 +84,11 @@ FDSNN_DEV void load_twist(double2 (&tw)[8], int t, const double2* __restrict__ t
     for (int r = 0; r < 8; ++r) tw[r] = __ldg(tables + t + r * (M / 8));
 }
 
-// TMEM layout per lane (128 columns): interior-pass twiddles of pass p at
-// columns (p-1)*32 (8 complex), twist factors at 96 (8 complex).  The two warps
-// sharing a TMEM lane quadrant (w and w+4) always have the same in-group
-// thread index t, hence identical constants, so one copy per lane suffices.
+// TMEM columns per lane (128 allocated): interior-pass twiddles of pass p at
+// (p-1)*32 (8 complex), twist factors at 96 (8 complex).  The warps sharing a
+// lane quadrant (w, w+4) have the same in-group index t, so one copy each.
 constexpr uint32_t PBS_TMEM_COLS = 128;
 constexpr uint32_t PBS_TMEM_TWIST = 96;
-
-template <int M>
-FDSNN_DEV void tmem_twist(uint32_t lane_base, double2 (&tw)[8]) {
-    double2 a[4];
-    tmem_ld4c(lane_base + PBS_TMEM_TWIST, a);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) tw[r] = a[r];
-    tmem_ld4c(lane_base + PBS_TMEM_TWIST + 16, a);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) tw[4 + r] = a[r];
-}
 
 template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN>
 __global__ void __launch_bounds__(PBS_THREADS, 1)
@@ -113,9 +106,9 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     constexpr int log2_2N = (M == 256) ? 10 : (M == 512) ? 11 : 12;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-    uint64_t* empty = full + S;
-    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem_raw + 96);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);   // key chunk landed
+    uint64_t* empty = full + 4;                                // ring stage free
+    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem_raw + 120);
     double2* ring = reinterpret_cast<double2*>(smem_raw + 128);
     const int warp = threadIdx.x / 32;
     const int g = threadIdx.x / T;
@@ -140,31 +133,26 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc(tmem_base_slot, PBS_TMEM_COLS);
-    // per-thread constants -> TMEM (lanes of warps 0-3 cover all quadrants)
-    if (warp < 4 && active) {
-        TwiddlesInRegs<M> twr;
-        load_twiddles<M>(twr.tw, t, args.tables + M);
-        double2 twist[8];
-        load_twist<M>(twist, t, args.tables);
-        tmem_fence_after();
-        __syncwarp();
-    }
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
-    const uint32_t lane_base = *tmem_base_slot + ((uint32_t)((warp % 4) * 32) << 16);
+    const uint32_t tbase = *tmem_base_slot;
+    const uint32_t lane_base = tbase + ((uint32_t)((warp % 4) * 32) << 16);
+
+    // ---- per-thread constants -> TMEM (warps 0-3 cover all lane quadrants)
     if (warp < 4 && active) {
         TwiddlesInRegs<M> twr;
         load_twiddles<M>(twr.tw, t, args.tables + M);
 #pragma unroll
         for (int p = 1; p < Schedule<M>::P; ++p) {
-            double d[8];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
+                double d[8];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    d[2 * r] = twr.tw.w[p][4 * h + r < 7 ? 4 * h + r : 6].x;
-                    d[2 * r + 1] = twr.tw.w[p][4 * h + r < 7 ? 4 * h + r : 6].y;
+                    const double2 w = twr.tw.w[p][4 * h + r < 7 ? 4 * h + r : 6];
+                    d[2 * r] = w.x;
+                    d[2 * r + 1] = w.y;
                 }
                 tmem_st16(lane_base + (p - 1) * 32 + 16 * h, d);
             }
@@ -183,55 +171,16 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
+
+    // ---- key ring: the producer (thread 0) fills S stages ahead; every
+    // consumer thread arrives on `empty` after its MAC, and the producer then
+    // refills that stage with chunk c+S.
     if (producer) {
         for (int s = 0; s < S && s < nchunks; ++s) {
             mbar_arrive_expect_tx(&full[s], CHUNK);
             bulk_g2s(ring + (size_t)s * 2 * M, args.bsk + (size_t)s * 2 * M, CHUNK, &full[s]);
         }
     }
-
-    if (active) {
-    const int64_t v = v0 + g;
-    const GroupSync gs{1 + g, T};
-    const TwiddlesInTmem<M> tw{lane_base};
-
-    // ---------------- setup: modulus switch + accumulator init -------------
-    if constexpr (!MODE_RAW) {
-        const int u = (int)(v / args.count);
-        const int64_t row = v - (int64_t)u * args.count;
-        const uint32_t* a_in = args.in + row * prm.stride;
-        const uint32_t* a_in2 = args.in2 ? args.in2 + row * prm.stride : nullptr;
-        for (int i = t; i < n; i += T) {
-            uint32_t a = a_in[i];
-            if (a_in2) a += a_in2[i];
-            a2N[i] = (uint16_t)rescale_q_to_2N(a, prm.log2q, log2_2N);
-        }
-        uint32_t b = a_in[n] + args.in_boff[u];
-        if (a_in2) b += a_in2[n];
-        const uint32_t b2N = (rescale_q_to_2N(b, prm.log2q, log2_2N) + prm.half_slot) & (2 * N - 1);
-        const int32_t* lut = args.lut[u];
-        // acc_b = X^{-b2N} * v  (monomial_rotate_raw with k = -b2N mod 2N)
-        for (int j = t; j < N; j += T) {
-            acc[j] = 0;
-            const int src = (j + (int)b2N) & (2 * N - 1);
-            const int32_t val = lut[src & (N - 1)];
-            acc[N + j] = (int32_t)((uint32_t)(src >= N ? -val : val) & qmask);
-        }
-    } else {
-        const int32_t* a_src = args.acc_io + v * 2 * N;
-        for (int j = t; j < 2 * N; j += T) acc[j] = (int32_t)((uint32_t)a_src[j] & qmask);
-        const int32_t* k_src = args.a2N_in + v * n;
-        for (int i = t; i < n; i += T) a2N[i] = (uint16_t)(k_src[i] & (2 * N - 1));
-    }
-    gs.sync();
-
-    const int bg = prm.bg_log;
-    const int32_t halfB1 = (1 << (bg - 1)) - 1;  // B/2 - 1
-    const int32_t bmask = (1 << bg) - 1;
-    int ex = 0;
-    double err_max = 0.0;
-
-    // release chunk c (all threads), and as producer refill its stage with c+S
     auto release = [&](int64_t c) {
         const int s = (int)(c % S);
         mbar_arrive(&empty[s]);
@@ -242,108 +191,155 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
         }
     };
 
-    int64_t c = 0;  // chunk counter = i * 2L + digit
-    for (int i = 0; i < n; ++i) {
-        const int k = a2N[i];
-        if (k == 0) {  // X^0*ACC - ACC = 0: identity step; keep the key ring in sync
-            for (int d = 0; d < 2 * L; ++d, ++c) {
-                mbar_wait(&full[c % S], (uint32_t)((c / S) & 1));
-                release(c);
-            }
-            continue;
-        }
-        double2 O0[8], O1[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) O0[r] = O1[r] = make_double2(0.0, 0.0);
+    if (active) {
+        const int64_t v = v0 + g;
+        const GroupSync gs{1 + g, T};
+        const TwiddlesInTmem<M> tw{lane_base};
 
-        for (int cc = 0; cc < 2; ++cc) {
-            const int32_t* a = acc + cc * N;
-            int32_t xlo[8], xhi[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-#pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    const int jj = t + r * T + half * M;
-                    const int s = (jj - k) & (2 * N - 1);
-                    const uint32_t val = (s >= N) ? (uint32_t)(-a[s - N]) : (uint32_t)a[s];
-                    const uint32_t d = (val - (uint32_t)a[jj]) & qmask;
-                    const int32_t xc = center_q(d, prm.log2q);
-                    if (half == 0) xlo[r] = xc; else xhi[r] = xc;
-                }
+        // ---------------- setup: modulus switch + accumulator init -------------
+        if constexpr (!MODE_RAW) {
+            const int u = (int)(v / args.count);
+            const int64_t row = v - (int64_t)u * args.count;
+            const uint32_t* a_in = args.in + row * prm.stride;
+            const uint32_t* a_in2 = args.in2 ? args.in2 + row * prm.stride : nullptr;
+            for (int i = t; i < n; i += T) {
+                uint32_t a = a_in[i];
+                if (a_in2) a += a_in2[i];
+                a2N[i] = (uint16_t)rescale_q_to_2N(a, prm.log2q, log2_2N);
             }
-            for (int lvl = 0; lvl < L; ++lvl, ++c) {
-                double2 vv[8];
-                {
-                    double2 twist[8];
-                    tmem_twist<M>(lane_base, twist);
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        const int32_t d1 = ((xlo[r] + halfB1) & bmask) - halfB1;
-                        const int32_t d2 = ((xhi[r] + halfB1) & bmask) - halfB1;
-                        xlo[r] = (xlo[r] - d1) >> bg;
-                        xhi[r] = (xhi[r] - d2) >> bg;
-                        vv[r] = cmul(make_double2((double)d1, (double)d2), twist[r]);
-                    }
-                }
-                fft_group<M, false>(vv, t, tw, buf0, buf1, ex, gs);
-                const int s = (int)(c % S);
-                mbar_wait(&full[s], (uint32_t)((c / S) & 1));
-                const double2* kd = ring + (size_t)s * 2 * M;
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    cmac(O0[r], vv[r], kd[t + r * T]);
-                    cmac(O1[r], vv[r], kd[M + t + r * T]);
-                }
-                release(c);
+            uint32_t b = a_in[n] + args.in_boff[u];
+            if (a_in2) b += a_in2[n];
+            const uint32_t b2N = (rescale_q_to_2N(b, prm.log2q, log2_2N) + prm.half_slot) & (2 * N - 1);
+            const int32_t* lut = args.lut[u];
+            // acc_b = X^{-b2N} * v  (monomial_rotate_raw with k = -b2N mod 2N)
+            for (int j = t; j < N; j += T) {
+                acc[j] = 0;
+                const int src = (j + (int)b2N) & (2 * N - 1);
+                const int32_t val = lut[src & (N - 1)];
+                acc[N + j] = (int32_t)((uint32_t)(src >= N ? -val : val) & qmask);
             }
-        }
-        fft_group2<M, true>(O0, O1, t, tw, buf0, buf1, gs);
-        {
-            double2 twist[8];
-            tmem_twist<M>(lane_base, twist);
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const int p = t + r * T;
-                const double2 z0 = cmulc(O0[r], twist[r]);
-                const double2 z1 = cmulc(O1[r], twist[r]);
-                const long long r00 = round_product(z0.x), r01 = round_product(z0.y);
-                const long long r10 = round_product(z1.x), r11 = round_product(z1.y);
-                if constexpr (TRACK_MARGIN) {
-                    err_max = fmax(err_max, fabs(z0.x - (double)r00));
-                    err_max = fmax(err_max, fabs(z0.y - (double)r01));
-                    err_max = fmax(err_max, fabs(z1.x - (double)r10));
-                    err_max = fmax(err_max, fabs(z1.y - (double)r11));
-                }
-                acc[p] = (int32_t)(((uint32_t)acc[p] + (uint32_t)r00) & qmask);
-                acc[p + M] = (int32_t)(((uint32_t)acc[p + M] + (uint32_t)r01) & qmask);
-                acc[N + p] = (int32_t)(((uint32_t)acc[N + p] + (uint32_t)r10) & qmask);
-                acc[N + p + M] = (int32_t)(((uint32_t)acc[N + p + M] + (uint32_t)r11) & qmask);
-            }
+        } else {
+            const int32_t* a_src = args.acc_io + v * 2 * N;
+            for (int j = t; j < 2 * N; j += T) acc[j] = (int32_t)((uint32_t)a_src[j] & qmask);
+            const int32_t* k_src = args.a2N_in + v * n;
+            for (int i = t; i < n; i += T) a2N[i] = (uint16_t)(k_src[i] & (2 * N - 1));
         }
         gs.sync();
-    }
-    if constexpr (TRACK_MARGIN) {
-        if (args.margin) atomicMax(args.margin, (unsigned long long)__double_as_longlong(err_max));
-    }
 
-    if constexpr (MODE_RAW) {
-        int32_t* a_dst = args.acc_io + v * 2 * N;
-        for (int j = t; j < 2 * N; j += T) a_dst[j] = acc[j];
-    } else {
-        // sample extract (bootstrap.py:484-488): (a_0, -a_{N-1}, ..., -a_1), b = acc_b[0]
-        uint32_t* out = args.ext_out + v * prm.ext_stride;
-        for (int j = t; j < N; j += T) {
-            const uint32_t a = (j == 0) ? (uint32_t)acc[0] : ((uint32_t)(-acc[N - j]) & qmask);
-            out[j] = a;
+        const int bg = prm.bg_log;
+        const int32_t halfB1 = (1 << (bg - 1)) - 1;  // B/2 - 1
+        const int32_t bmask = (1 << bg) - 1;
+        int ex = 0;
+        double err_max = 0.0;
+
+        int64_t c = 0;  // chunk counter = i * 2L + digit
+        for (int i = 0; i < n; ++i) {
+            const int k = a2N[i];
+            if (k == 0) {  // X^0*ACC - ACC = 0: identity step; keep the key pipeline in sync
+                for (int d = 0; d < 2 * L; ++d, ++c) {
+                    mbar_wait(&full[c % S], (uint32_t)((c / S) & 1));
+                    release(c);
+                }
+                continue;
+            }
+            double2 O0[8], O1[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) O0[r] = O1[r] = make_double2(0.0, 0.0);
+
+            for (int cc = 0; cc < 2; ++cc) {
+                const int32_t* a = acc + cc * N;
+                int32_t xlo[8], xhi[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        const int jj = t + r * T + half * M;
+                        const int s = (jj - k) & (2 * N - 1);
+                        const uint32_t val = (s >= N) ? (uint32_t)(-a[s - N]) : (uint32_t)a[s];
+                        const uint32_t d = (val - (uint32_t)a[jj]) & qmask;
+                        const int32_t xc = center_q(d, prm.log2q);
+                        if (half == 0) xlo[r] = xc; else xhi[r] = xc;
+                    }
+                }
+                for (int lvl = 0; lvl < L; ++lvl, ++c) {
+                    double2 vv[8];
+                    {
+                        uint32_t twr[32];
+                        tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
+                        int32_t d1[8], d2[8];
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            d1[r] = ((xlo[r] + halfB1) & bmask) - halfB1;
+                            d2[r] = ((xhi[r] + halfB1) & bmask) - halfB1;
+                            xlo[r] = (xlo[r] - d1[r]) >> bg;
+                            xhi[r] = (xhi[r] - d2[r]) >> bg;
+                        }
+                        tmem_wait32(twr);
+#pragma unroll
+                        for (int r = 0; r < 8; ++r)
+                            vv[r] = cmul(make_double2((double)d1[r], (double)d2[r]), words_c(twr, r));
+                    }
+                    fft_group<M, false>(vv, t, tw, buf0, buf1, ex, gs);
+                    const int s = (int)(c % S);
+                    mbar_wait(&full[s], (uint32_t)((c / S) & 1));
+                    const double2* kd = ring + (size_t)s * 2 * M;
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        cmac(O0[r], vv[r], kd[t + r * T]);
+                        cmac(O1[r], vv[r], kd[M + t + r * T]);
+                    }
+                    release(c);
+                }
+            }
+            {
+                uint32_t twr[32];
+                auto fetch_twist = [&]() { tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr); };
+                fft_group2<M, true>(O0, O1, t, tw, buf0, buf1, gs, fetch_twist);
+                tmem_wait32(twr);
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int p = t + r * T;
+                    const double2 tr = words_c(twr, r);
+                    const double2 z0 = cmulc(O0[r], tr);
+                    const double2 z1 = cmulc(O1[r], tr);
+                    const long long r00 = round_product(z0.x), r01 = round_product(z0.y);
+                    const long long r10 = round_product(z1.x), r11 = round_product(z1.y);
+                    if constexpr (TRACK_MARGIN) {
+                        err_max = fmax(err_max, fabs(z0.x - (double)r00));
+                        err_max = fmax(err_max, fabs(z0.y - (double)r01));
+                        err_max = fmax(err_max, fabs(z1.x - (double)r10));
+                        err_max = fmax(err_max, fabs(z1.y - (double)r11));
+                    }
+                    acc[p] = (int32_t)(((uint32_t)acc[p] + (uint32_t)r00) & qmask);
+                    acc[p + M] = (int32_t)(((uint32_t)acc[p + M] + (uint32_t)r01) & qmask);
+                    acc[N + p] = (int32_t)(((uint32_t)acc[N + p] + (uint32_t)r10) & qmask);
+                    acc[N + p + M] = (int32_t)(((uint32_t)acc[N + p + M] + (uint32_t)r11) & qmask);
+                }
+            }
+            gs.sync();
         }
-        if (t == 0) out[N] = (uint32_t)acc[N];
-    }
+        if constexpr (TRACK_MARGIN) {
+            if (args.margin) atomicMax(args.margin, (unsigned long long)__double_as_longlong(err_max));
+        }
+
+        if constexpr (MODE_RAW) {
+            int32_t* a_dst = args.acc_io + v * 2 * N;
+            for (int j = t; j < 2 * N; j += T) a_dst[j] = acc[j];
+        } else {
+            // sample extract (bootstrap.py:484-488): (a_0, -a_{N-1}, ..., -a_1), b = acc_b[0]
+            uint32_t* out = args.ext_out + v * prm.ext_stride;
+            for (int j = t; j < N; j += T) {
+                const uint32_t a = (j == 0) ? (uint32_t)acc[0] : ((uint32_t)(-acc[N - j]) & qmask);
+                out[j] = a;
+            }
+            if (t == 0) out[N] = (uint32_t)acc[N];
+        }
     }  // active
     tmem_fence_before();
     __syncthreads();
     if (warp == 0) {
         tmem_fence_after();
-        tmem_dealloc(*tmem_base_slot, PBS_TMEM_COLS);
+        tmem_dealloc(tbase, PBS_TMEM_COLS);
     }
 }
 
