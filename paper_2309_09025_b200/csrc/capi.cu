@@ -19,6 +19,10 @@
 
 using namespace fdsnn;
 
+#ifndef FDSNN_G512
+#define FDSNN_G512 4  // accumulators per CTA at N=1024
+#endif
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -151,7 +155,7 @@ int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_
     TimerScope ts(ctx, 0, s);
     switch (ctx->dp.M) {
         case 256: return launch_br_m<256, 8>(ctx, a, V, raw, s);
-        case 512: return launch_br_m<512, 4>(ctx, a, V, raw, s);
+        case 512: return launch_br_m<512, FDSNN_G512>(ctx, a, V, raw, s);
         case 1024: return launch_br_m<1024, 2>(ctx, a, V, raw, s);
     }
     return set_err(FDSNN_ERR_PARAMETER, "unsupported ring degree N=%d", ctx->dp.N);

@@ -84,16 +84,20 @@ FDSNN_DEV void load_twist(double2 (&tw)[8], int t, const double2* __restrict__ t
     for (int r = 0; r < 8; ++r) tw[r] = __ldg(tables + t + r * (M / 8));
 }
 
-// TMEM columns per lane (128 allocated): interior-pass twiddles of pass p at
-// (p-1)*32 (8 complex), twist factors at 96 (8 complex).  The warps sharing a
-// lane quadrant (w, w+4) have the same in-group index t, so one copy each.
-constexpr uint32_t PBS_TMEM_COLS = 128;
+// TMEM columns per lane (256 allocated): interior-pass twiddles of pass p at
+// (p-1)*32 (8 complex), twist factors at 96 (8 complex) -- the warps sharing a
+// lane quadrant (w, w+4) have the same in-group index t, so one copy each --
+// and at 128 + 32*(w/4) the thread's own accumulator coefficients
+// acc[c][t + rT + h*M] (word 16c + 8h + r): the unrotated operand of
+// (X^k - 1)*ACC and the read half of the accumulator update come from TMEM,
+// so shared memory only serves the rotated reads and the update stores.
+constexpr uint32_t PBS_TMEM_COLS = 256;
 constexpr uint32_t PBS_TMEM_TWIST = 96;
+constexpr uint32_t PBS_TMEM_OWN = 128;
 
 template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN>
-__global__ void __launch_bounds__(PBS_THREADS, 1)
+__global__ void __launch_bounds__(G * (M / 8), 1)
 pbs_blind_rotate_kernel(const PbsArgs args) {
-    static_assert(G * (M / 8) == PBS_THREADS, "CTA shape");
     constexpr int T = M / 8;
     constexpr int PADM = PbsShape<M>::PADM;
     constexpr int S = PbsRing<M>::S;
@@ -225,6 +229,18 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
             for (int i = t; i < n; i += T) a2N[i] = (uint16_t)(k_src[i] & (2 * N - 1));
         }
         gs.sync();
+        const uint32_t own_col = lane_base + PBS_TMEM_OWN + 32 * (uint32_t)(warp / 4);
+        {
+            uint32_t w[32];
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) w[16 * cc + 8 * h + r] = (uint32_t)acc[cc * N + t + r * T + h * M];
+            tmem_st32(own_col, w);
+            tmem_wait_st();
+        }
 
         const int bg = prm.bg_log;
         const int32_t halfB1 = (1 << (bg - 1)) - 1;  // B/2 - 1
@@ -249,17 +265,23 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
             for (int cc = 0; cc < 2; ++cc) {
                 const int32_t* a = acc + cc * N;
                 int32_t xlo[8], xhi[8];
+                uint32_t ow[16];
+                tmem_ld16_async(own_col + 16 * cc, ow);
+                uint32_t rv[16];
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {
                         const int jj = t + r * T + half * M;
                         const int s = (jj - k) & (2 * N - 1);
-                        const uint32_t val = (s >= N) ? (uint32_t)(-a[s - N]) : (uint32_t)a[s];
-                        const uint32_t d = (val - (uint32_t)a[jj]) & qmask;
-                        const int32_t xc = center_q(d, prm.log2q);
-                        if (half == 0) xlo[r] = xc; else xhi[r] = xc;
+                        rv[8 * half + r] = (s >= N) ? (uint32_t)(-a[s - N]) : (uint32_t)a[s];
                     }
+                }
+                tmem_wait16(ow);
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    xlo[r] = center_q((rv[r] - ow[r]) & qmask, prm.log2q);
+                    xhi[r] = center_q((rv[8 + r] - ow[8 + r]) & qmask, prm.log2q);
                 }
                 for (int lvl = 0; lvl < L; ++lvl, ++c) {
                     double2 vv[8];
@@ -292,10 +314,14 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                 }
             }
             {
-                uint32_t twr[32];
-                auto fetch_twist = [&]() { tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr); };
-                fft_group2<M, true>(O0, O1, t, tw, buf0, buf1, gs, fetch_twist);
+                uint32_t twr[32], own[32];
+                auto fetch = [&]() {
+                    tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
+                    tmem_ld32_async(own_col, own);
+                };
+                fft_group2<M, true>(O0, O1, t, tw, buf0, buf1, gs, fetch);
                 tmem_wait32(twr);
+                tmem_touch32(own);
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
                     const int p = t + r * T;
@@ -310,11 +336,17 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                         err_max = fmax(err_max, fabs(z1.x - (double)r10));
                         err_max = fmax(err_max, fabs(z1.y - (double)r11));
                     }
-                    acc[p] = (int32_t)(((uint32_t)acc[p] + (uint32_t)r00) & qmask);
-                    acc[p + M] = (int32_t)(((uint32_t)acc[p + M] + (uint32_t)r01) & qmask);
-                    acc[N + p] = (int32_t)(((uint32_t)acc[N + p] + (uint32_t)r10) & qmask);
-                    acc[N + p + M] = (int32_t)(((uint32_t)acc[N + p + M] + (uint32_t)r11) & qmask);
+                    own[r] = (own[r] + (uint32_t)r00) & qmask;
+                    own[8 + r] = (own[8 + r] + (uint32_t)r01) & qmask;
+                    own[16 + r] = (own[16 + r] + (uint32_t)r10) & qmask;
+                    own[24 + r] = (own[24 + r] + (uint32_t)r11) & qmask;
+                    acc[p] = (int32_t)own[r];
+                    acc[p + M] = (int32_t)own[8 + r];
+                    acc[N + p] = (int32_t)own[16 + r];
+                    acc[N + p + M] = (int32_t)own[24 + r];
                 }
+                tmem_st32(own_col, own);
+                tmem_wait_st();
             }
             gs.sync();
         }

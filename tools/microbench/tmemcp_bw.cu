@@ -13,11 +13,11 @@ __device__ __forceinline__ uint64_t sdesc(const void* p) {
 }
 template <int SHAPE>
 __global__ void k(uint32_t* out, int iters, long long* cyc) {
-    extern __shared__ __align__(1024) uint32_t blk[];  // 16 KB
+    extern __shared__ __align__(1024) uint32_t blk[];  // 32 KB
     __shared__ uint32_t tbase;
     __shared__ __align__(8) uint64_t bar;
     const int warp = threadIdx.x / 32;
-    for (int i = threadIdx.x; i < 4096; i += blockDim.x) blk[i] = i;
+    for (int i = threadIdx.x; i < 8192; i += blockDim.x) blk[i] = i;
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
         asm volatile("fence.mbarrier_init.release.cluster;");
@@ -35,11 +35,19 @@ __global__ void k(uint32_t* out, int iters, long long* cyc) {
     if (threadIdx.x == 0) {
         for (int it = 0; it < iters; ++it) {
             for (int b = 0; b < 16; ++b) {
-                uint64_t d = sdesc(&blk[b * 256]);
-                if (SHAPE == 0)
+                if (SHAPE == 0) {
+                    uint64_t d = sdesc(&blk[b * 256]);  // 1 KB block -> 2 KB written (multicast)
                     asm volatile("tcgen05.cp.cta_group::1.64x128b.warpx2::02_13 [%0], %1;" ::"r"(tb + 4 * b), "l"(d) : "memory");
-                else
+                } else if (SHAPE == 1) {
+                    uint64_t d = sdesc(&blk[b * 512]);  // 2 KB block
                     asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(tb + 4 * b), "l"(d) : "memory");
+                } else if (SHAPE == 2) {
+                    uint64_t d = sdesc(&blk[(b % 8) * 1024]);  // 4 KB block (128 rows x 32 B)
+                    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tb + 8 * (b % 8)), "l"(d) : "memory");
+                } else {
+                    uint64_t d = sdesc(&blk[b * 128]);  // 512 B block -> 2 KB written (x4 multicast)
+                    asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tb + 4 * b), "l"(d) : "memory");
+                }
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)) : "memory");
             asm volatile("{\n\t.reg .pred P1;\nW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra W;\n\t}" ::"r"(su32(&bar)), "r"(it & 1) : "memory");
@@ -53,13 +61,18 @@ __global__ void k(uint32_t* out, int iters, long long* cyc) {
 }
 int main() {
     uint32_t* d; long long* c; cudaMalloc(&d, 64); cudaMalloc(&c, 8);
-    for (int shape = 0; shape < 2; ++shape) {
+    const double bytes_per_iter[4] = {16384, 32768, 32768, 8192};  // smem bytes read per iteration
+    for (int shape = 0; shape < 4; ++shape) {
         for (int iters : {1, 100}) {
-            if (shape == 0) k<0><<<148, 128, 16384>>>(d, iters, c); else k<1><<<148, 128, 16384>>>(d, iters, c);
+            if (shape == 0) k<0><<<148, 128, 32768>>>(d, iters, c);
+            if (shape == 1) k<1><<<148, 128, 32768>>>(d, iters, c);
+            if (shape == 2) k<2><<<148, 128, 32768>>>(d, iters, c);
+            if (shape == 3) k<3><<<148, 128, 32768>>>(d, iters, c);
             cudaError_t e = cudaDeviceSynchronize();
             long long h; cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
-            printf("shape %d iters %d: %lld cycles total, %.0f cycles per 16KB chunk (%.1f B/clk) %s\n", shape, iters, h,
-                   (double)h / iters, 16384.0 * iters / h, cudaGetErrorString(e));
+            printf("shape %d iters %d: %.0f cycles per iter, smem read %.1f B/clk %s\n", shape, iters,
+                   (double)h / iters, bytes_per_iter[shape] * iters / h, cudaGetErrorString(e));
+            if (e != cudaSuccess) return 1;
         }
     }
 }
