@@ -96,6 +96,16 @@ def dist_setup():
     return world, rank, local
 
 
+def shard_range(total: int, rank: int, world: int):
+    """Contiguous [lo, hi) share of `total` independent items for `rank` (replica /
+    sample sharding: PBS batches and images are independent, no collective)."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world of {world}")
+    base, extra = divmod(total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
 def max_over_ranks(x: float, world: int, device=None) -> float:
     if world == 1:
         return x

@@ -1,0 +1,101 @@
+"""GPU edge cases: empty and ragged batches, identity rotations, error
+behaviour, determinism, and the FP64 exactness margin of the transform."""
+import numpy as np
+import pytest
+
+from conftest import O, oracle_key
+from paper_2309_09025_b200 import bootstrap, errors, lwe, network, neuron
+
+pytestmark = pytest.mark.gpu
+
+
+def test_empty_batches(desk, desk_keys):
+    sk, _, bsk = desk_keys
+    A = np.zeros((0, desk.n), np.int64)
+    b = np.zeros(0, np.int64)
+    oA, ob = bootstrap.bootstrap_batch(neuron.g_fire(desk.p), A, b, bsk)
+    assert oA.shape == (0, desk.n) and ob.shape == (0,)
+    out = neuron.fhe_lif_step_batch(A, b, A, b, neuron.LifParams(tau=2, theta=64), bsk)
+    assert all(x.shape[0] == 0 for x in out)
+
+
+@pytest.mark.parametrize("count", [1, 3, 5, 7])
+def test_ragged_batches_match_oracle(desk, desk_keys, count):
+    """Batch sizes that leave part of the last CTA idle."""
+    sk, _, bsk = desk_keys
+    rng = np.random.default_rng(count)
+    ms = rng.integers(-511, 513, count)
+    A, b = lwe.encrypt_batch(ms, sk, desk, rng)
+    g = neuron.g_fire(desk.p)
+    oA, ob = bootstrap.bootstrap_batch(g, A, b, bsk)
+    wA, wb = O.bootstrap_batch(g.table, A, b, oracle_key(desk, bsk))
+    assert np.array_equal(oA, wA) and np.array_equal(ob, wb)
+
+
+def test_identity_rotation_steps(toy, toy_keys):
+    """Masks with many zero coordinates exercise the k == 0 skip path per ciphertext."""
+    sk, _, bsk = toy_keys
+    rng = np.random.default_rng(2)
+    acc = rng.integers(0, toy.q, (9, 2, toy.N))
+    a2N = rng.integers(0, 2 * toy.N, (9, toy.n))
+    a2N[:, ::2] = 0
+    a2N[3] = 0
+    got = bootstrap.blind_rotate_batch(acc, a2N, bsk)
+    assert np.array_equal(got, O.blind_rotate(acc, a2N, oracle_key(toy, bsk)))
+    assert np.array_equal(got[3], acc[3])
+
+
+def test_deterministic(desk, desk_keys):
+    sk, _, bsk = desk_keys
+    rng = np.random.default_rng(5)
+    A, b = lwe.encrypt_batch(rng.integers(-511, 513, 33), sk, desk, rng)
+    g = neuron.g_fire(desk.p)
+    r1 = bootstrap.bootstrap_batch(g, A, b, bsk)
+    r2 = bootstrap.bootstrap_batch(g, A, b, bsk)
+    assert np.array_equal(r1[0], r2[0]) and np.array_equal(r1[1], r2[1])
+
+
+def test_parameter_errors(desk, desk_keys):
+    sk, _, bsk = desk_keys
+    g = neuron.g_fire(desk.p)
+    with pytest.raises(errors.ParameterError):
+        bootstrap.bootstrap_batch(g, np.zeros((2, desk.n + 1), np.int64), np.zeros(2, np.int64), bsk)
+    with pytest.raises(errors.ParameterError):
+        bootstrap.bootstrap_batch(neuron.g_fire(64), np.zeros((2, desk.n), np.int64), np.zeros(2, np.int64), bsk)
+    with pytest.raises(errors.ParameterError):
+        bootstrap.key_switch_batch(np.zeros((1, 10), np.int64), np.zeros(1, np.int64), bsk.ksk, desk)
+    layer = network.WeightLayer("linear", np.ones((3, 4), np.int64), None, 1.0, (3,))
+    x = network.zero_states(5, desk)
+    with pytest.raises(errors.ParameterError):
+        network.layer_forward(x, layer, desk)
+
+
+@pytest.mark.parametrize("which,bound", [("desk", 0.01), ("c4prm", 0.01)])
+def test_transform_exactness_margin(which, bound, request):
+    """max |x - round(x)| over every rounded product of every CMux step stays far
+    below 0.5 (the condition under which FP64 transforms are exact and the
+    device's round-to-nearest equals the reference's round-half-away)."""
+    prm = request.getfixturevalue(which)
+    sk, _, bsk = request.getfixturevalue("desk_keys" if which == "desk" else "c4_keys")
+    rng = np.random.default_rng(9)
+    A, b = lwe.encrypt_batch(rng.integers(-prm.p // 2 + 1, prm.p // 2 + 1, 64), sk, prm, rng)
+    dev = bsk.device
+    dev.margin(True)
+    try:
+        bootstrap.bootstrap_batch(neuron.g_fire(prm.p), A, b, bsk)
+        m = dev.margin()
+    finally:
+        dev.margin(False)
+    assert 0.0 < m < bound, m
+
+
+def test_device_rows_roundtrip(desk, desk_keys):
+    sk, _, bsk = desk_keys
+    rng = np.random.default_rng(11)
+    A = rng.integers(-desk.q, 2 * desk.q, (17, desk.n))
+    b = rng.integers(-desk.q, 2 * desk.q, 17)
+    dev = bsk.device
+    rows = dev.rows_from_host(A, b)
+    A2, b2 = dev.rows_to_host(rows)
+    assert np.array_equal(A2, A % desk.q) and np.array_equal(b2, b % desk.q)
+    assert rows.shape == (17, 516)
