@@ -152,7 +152,8 @@ FDSNN_DEV void load_twiddles(Twiddles<M>& tw, int t, const double2* __restrict__
 // Twiddle providers.  issue<PASS>(raw) starts fetching the R-1 factors
 // e^{2 pi i r jm/(NS R)} of this thread's interior pass PASS; finish<PASS>
 // (raw, w) completes the fetch into w[r-1].  The FFT issues the fetch before
-// the pass's shared-memory exchange so its latency hides behind the barrier.
+// the pass's exchange stores and completes it before the barrier, so the
+// barrier wait hides its latency and the exchange loads issue right after it.
 template <int M>
 struct TwiddlesInRegs {
     Twiddles<M> tw;
@@ -247,11 +248,11 @@ FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
         tw.template issue<PS>(raw);                               \
         double2* b = ex ? buf1 : buf0;                            \
         pass_store<M, PS - 1>(v, t, b);                           \
+        double2 w[8];                                             \
+        tw.template finish<PS>(raw, w);                           \
         gs.sync();                                                \
         pass_load<M, PS>(v, t, b);                                \
         ex ^= 1;                                                  \
-        double2 w[8];                                             \
-        tw.template finish<PS>(raw, w);                           \
         if constexpr (PS == P - 1) pre_last();                    \
         pass_body<M, PS, INV>(v, w);                              \
     }
@@ -282,11 +283,11 @@ FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& t
         gs.sync();                                                \
         pass_store<M, PS - 1>(v0, t, buf0);                       \
         pass_store<M, PS - 1>(v1, t, buf1);                       \
+        double2 w[8];                                             \
+        tw.template finish<PS>(raw, w);                           \
         gs.sync();                                                \
         pass_load<M, PS>(v0, t, buf0);                            \
         pass_load<M, PS>(v1, t, buf1);                            \
-        double2 w[8];                                             \
-        tw.template finish<PS>(raw, w);                           \
         if constexpr (PS == P - 1) pre_last();                    \
         pass_body<M, PS, INV>(v0, w);                             \
         pass_body<M, PS, INV>(v1, w);                             \
