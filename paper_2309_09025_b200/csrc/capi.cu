@@ -16,7 +16,6 @@
 #include "keyswitch.cuh"
 #include "linear.cuh"
 #include "pbs.cuh"
-#include "pbs_warp.cuh"
 
 using namespace fdsnn;
 
@@ -151,30 +150,9 @@ int launch_br_m(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStrea
                              : launch_br_t<M, G, false, false>(ctx, a, V, s);
 }
 
-template <bool MARGIN>
-int launch_brw_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_t s) {
-    const size_t smem = pbsw_smem_bytes(ctx->dp.n);
-    auto kern = pbs_warp_kernel<MARGIN>;
-    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)((V + 7) / 8), PBSW_THREADS, smem, s>>>(a);
-    CU(cudaGetLastError());
-    return FDSNN_OK;
-}
-
-bool use_warp_kernel() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("FDSNN_BR_KERNEL");
-        v = (e && std::string(e) == "group") ? 0 : 1;
-    }
-    return v == 1;
-}
-
 int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_t s) {
     if (V <= 0) return FDSNN_OK;
     TimerScope ts(ctx, 0, s);
-    if (ctx->dp.M == 512 && !raw && use_warp_kernel())
-        return ctx->track_margin ? launch_brw_t<true>(ctx, a, V, s) : launch_brw_t<false>(ctx, a, V, s);
     switch (ctx->dp.M) {
         case 256: return launch_br_m<256, 8>(ctx, a, V, raw, s);
         case 512: return launch_br_m<512, FDSNN_G512>(ctx, a, V, raw, s);

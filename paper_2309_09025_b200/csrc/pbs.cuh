@@ -249,9 +249,6 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
         double err_max = 0.0;
 
         int64_t c = 0;  // chunk counter = i * 2L + digit
-#ifdef FDSNN_PHASE_DELAY
-        if (g >= G / 2) __nanosleep(FDSNN_PHASE_DELAY);
-#endif
         for (int i = 0; i < n; ++i) {
             const int k = a2N[i];
             if (k == 0) {  // X^0*ACC - ACC = 0: identity step; keep the key pipeline in sync
