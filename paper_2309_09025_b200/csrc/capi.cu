@@ -19,9 +19,6 @@
 
 using namespace fdsnn;
 
-#ifndef FDSNN_G512
-#define FDSNN_G512 4  // accumulators per CTA at N=1024
-#endif
 
 namespace {
 
@@ -155,7 +152,12 @@ int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_
     TimerScope ts(ctx, 0, s);
     switch (ctx->dp.M) {
         case 256: return launch_br_m<256, 8>(ctx, a, V, raw, s);
-        case 512: return launch_br_m<512, FDSNN_G512>(ctx, a, V, raw, s);
+        case 512:
+            // accumulators per CTA: 4 amortises each key chunk over 4 rotations;
+            // small batches spread over more SMs instead (latency-bound regime)
+            // (G=1 CTAs are small enough for 2 per SM: <= 296 rotations fit in one wave)
+            if (V > 2 * 148) return launch_br_m<512, 4>(ctx, a, V, raw, s);
+            return launch_br_m<512, 1>(ctx, a, V, raw, s);
         case 1024: return launch_br_m<1024, 2>(ctx, a, V, raw, s);
     }
     return set_err(FDSNN_ERR_PARAMETER, "unsupported ring degree N=%d", ctx->dp.N);

@@ -1,0 +1,64 @@
+"""Throughput of configs 2-4 on the device (development/report aid):
+config 3 PBS sweep, config 2 (32 images, T=4) and config 4 (C4 params, T=8)
+encrypted inferences per second, and the C4 LIF PBS rate."""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+import numpy as np
+import torch
+import workloads as W
+import paper_2309_09025_b200 as api
+from paper_2309_09025_b200 import bootstrap, network, neuron
+
+out = {}
+which = sys.argv[1:] or ["c3", "c2", "c4"]
+if "c3" in which or "c2" in which:
+    prm = W.desk1024(api)
+    sk, zk, bsk = W.keys(api, prm)
+    dev = bsk.device
+    g = neuron.g_fire(prm.p)
+    lut = dev.lut(bootstrap.test_polynomial(g, prm))
+if "c3" in which:
+    sweep = {}
+    for B in (1, 64, 1024, 16384, 131072):
+        ms = W.pbs_messages(prm, B, seed=B)
+        A, b = W.encrypt(api, prm, sk, ms)
+        rows = dev.rows_from_host(A, b)
+        dev.pbs_dev([lut], [0], [0], rows)
+        torch.cuda.synchronize()
+        reps = 3 if B <= 16384 else 1
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            dev.pbs_dev([lut], [0], [0], rows)
+        e1.record(); torch.cuda.synchronize()
+        ms_ = e0.elapsed_time(e1) / reps
+        sweep[B] = {"ms": ms_, "pbs_per_s": B / ms_ * 1e3}
+    out["config3_sweep"] = sweep
+if "c2" in which:
+    lif = W.lif_for(api, prm)
+    net = W.config2_network(api, lif)
+    imgs = W.synth_images(32)
+    encs = W.encrypt_images(api, prm, sk, imgs)
+    network.infer_batch(encs[:2], net, bsk)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    scores, stats = network.infer_batch(encs, net, bsk)
+    dt = time.perf_counter() - t0
+    out["config2"] = {"images": 32, "seconds": dt, "inferences_per_s": 32 / dt, "pbs": stats.bootstrap_count,
+                      "pbs_per_s": stats.bootstrap_count / dt}
+if "c4" in which:
+    prm4 = W.c4_params(api)
+    sk4, zk4, bsk4 = W.keys(api, prm4)
+    lif4 = W.lif_for(api, prm4)
+    net4 = W.config4_network(api, lif4)
+    imgs = W.synth_images(32)
+    encs = W.encrypt_images(api, prm4, sk4, imgs)
+    network.infer_batch(encs[:1], net4, bsk4, T=1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    scores, stats = network.infer_batch(encs, net4, bsk4)
+    dt = time.perf_counter() - t0
+    out["config4"] = {"images": 32, "seconds": dt, "inferences_per_s": 32 / dt, "pbs": stats.bootstrap_count,
+                      "pbs_per_s": stats.bootstrap_count / dt}
+print(json.dumps(out))
