@@ -69,6 +69,20 @@ void* fdsnn_ctx_stream(fdsnn_ctx* ctx);
 int fdsnn_bsk_load(fdsnn_ctx* ctx, const int64_t* rows, const int64_t* ksk_A,
                    const int64_t* ksk_b);
 
+/* Load the bootstrapping key straight from a reference "FDSN" BK container
+ * (serial.save_bootstrap_key, reference serial.py:111-118): arrays ek_a,
+ * ek_b (n, 2l, N), ksk_A, ksk_b.  `params_digest` (hex, may be NULL) must
+ * equal FheParams.digest() of the context's parameters (serial.py:79-84). */
+int fdsnn_bsk_load_fdsn(fdsnn_ctx* ctx, const char* path, const char* params_digest);
+
+/* Read a reference "FDSN" CT container (serial.save_ciphertexts,
+ * serial.py:132-137).  Always returns the ciphertext count and the tensor
+ * shape (ndim <= 8); when d_rows is non-NULL also uploads the ciphertexts as
+ * device rows (count * fdsnn_row_stride(n) words). */
+int fdsnn_ciphertexts_load_fdsn(fdsnn_ctx* ctx, const char* path, const char* params_digest,
+                                int64_t* count, int32_t* ndim, int64_t* shape,
+                                uint32_t* d_rows, void* stream);
+
 /* Register a test polynomial (bootstrap.test_polynomial, bootstrap.py:283-289):
  * N int64 residues.  Returns a LUT id usable by the PBS entry points. */
 int fdsnn_lut_load(fdsnn_ctx* ctx, const int64_t* testpoly, int32_t* lut_id);

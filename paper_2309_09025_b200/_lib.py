@@ -43,6 +43,9 @@ SIGNATURES = {
     "fdsnn_ctx_destroy": (_c_int, [_vp]),
     "fdsnn_ctx_stream": (_vp, [_vp]),
     "fdsnn_bsk_load": (_c_int, [_vp, _vp, _vp, _vp]),
+    "fdsnn_bsk_load_fdsn": (_c_int, [_vp, ctypes.c_char_p, ctypes.c_char_p]),
+    "fdsnn_ciphertexts_load_fdsn": (_c_int, [_vp, ctypes.c_char_p, ctypes.c_char_p, _i64p, _i32p,
+                                             _i64p, _vp, _vp]),
     "fdsnn_lut_load": (_c_int, [_vp, _vp, _i32p]),
     "fdsnn_pbs_batch": (_c_int, [_vp, _i32, _vp, _vp, _i64, _vp, _vp]),
     "fdsnn_lif_step_batch": (_c_int, [_vp, _i32, _i32, _i64, _vp, _vp, _vp, _vp, _i64,

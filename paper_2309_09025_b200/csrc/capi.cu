@@ -12,7 +12,10 @@
 #include <string>
 #include <vector>
 
+#include <map>
+
 #include "../../include/fdsnn_b200.h"
+#include "fdsn.h"
 #include "keyswitch.cuh"
 #include "linear.cuh"
 #include "pbs.cuh"
@@ -414,6 +417,54 @@ int fdsnn_bsk_load(fdsnn_ctx* ctx, const int64_t* rows, const int64_t* ksk_A, co
     CU(cudaFree(d_rows));
     ctx->keys_loaded = true;
     return FDSNN_OK;
+}
+
+int fdsnn_bsk_load_fdsn(fdsnn_ctx* ctx, const char* path, const char* params_digest) {
+    if (!ctx || !path) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+    std::map<std::string, FdsnArray> arrs;
+    const std::string err = fdsn_read(path, "BK", params_digest, arrs);
+    if (!err.empty()) return set_err(FDSNN_ERR_PARAMETER, "%s: %s", path, err.c_str());
+    const DevParams& d = ctx->dp;
+    auto shape_is = [&](const char* name, std::vector<int64_t> want) {
+        auto it = arrs.find(name);
+        return it != arrs.end() && it->second.shape == want;
+    };
+    const int64_t kr = (int64_t)d.N * d.ks_L;
+    if (!shape_is("ek_a", {d.n, 2 * d.L, d.N}) || !shape_is("ek_b", {d.n, 2 * d.L, d.N}) ||
+        !shape_is("ksk_A", {kr, d.n}) || !shape_is("ksk_b", {kr}))
+        return set_err(FDSNN_ERR_PARAMETER, "%s: key arrays do not match the parameters", path);
+    // rows (n, 2l, 2, N): [i][row][a|b][coef]
+    const auto& ea = arrs["ek_a"].data;
+    const auto& eb = arrs["ek_b"].data;
+    std::vector<int64_t> rows((size_t)d.n * 2 * d.L * 2 * d.N);
+    const size_t poly = (size_t)d.N;
+    for (size_t r = 0; r < (size_t)d.n * 2 * d.L; ++r) {
+        std::memcpy(&rows[(2 * r) * poly], &ea[r * poly], poly * 8);
+        std::memcpy(&rows[(2 * r + 1) * poly], &eb[r * poly], poly * 8);
+    }
+    return fdsnn_bsk_load(ctx, rows.data(), arrs["ksk_A"].data.data(), arrs["ksk_b"].data.data());
+}
+
+int fdsnn_ciphertexts_load_fdsn(fdsnn_ctx* ctx, const char* path, const char* params_digest,
+                                int64_t* count, int32_t* ndim, int64_t* shape, uint32_t* d_rows,
+                                void* stream) {
+    if (!ctx || !path || !count) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+    std::map<std::string, FdsnArray> arrs;
+    const std::string err = fdsn_read(path, "CT", params_digest, arrs);
+    if (!err.empty()) return set_err(FDSNN_ERR_PARAMETER, "%s: %s", path, err.c_str());
+    if (!arrs.count("A") || !arrs.count("b") || !arrs.count("shape"))
+        return set_err(FDSNN_ERR_PARAMETER, "%s: missing arrays", path);
+    const FdsnArray& A = arrs["A"];
+    const FdsnArray& b = arrs["b"];
+    const int64_t cnt = b.shape.empty() ? 0 : b.shape[0];
+    if (A.shape.size() != 2 || A.shape[0] != cnt || A.shape[1] != ctx->dp.n)
+        return set_err(FDSNN_ERR_PARAMETER, "%s: mask array does not match n=%d", path, ctx->dp.n);
+    *count = cnt;
+    const FdsnArray& sh = arrs["shape"];
+    if (ndim) *ndim = (int32_t)sh.data.size();
+    if (shape) for (size_t i = 0; i < sh.data.size() && i < 8; ++i) shape[i] = sh.data[i];
+    if (!d_rows) return FDSNN_OK;
+    return fdsnn_rows_from_host(ctx, A.data.data(), b.data.data(), cnt, d_rows, stream);
 }
 
 int fdsnn_lut_load(fdsnn_ctx* ctx, const int64_t* testpoly, int32_t* lut_id) {

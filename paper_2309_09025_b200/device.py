@@ -76,6 +76,24 @@ class DeviceContext:
         _lib.check(self.lib.fdsnn_bsk_load(self.h, _ptr(rows), _ptr(ksk_A), _ptr(ksk_b)))
         self.keys_loaded = True
 
+    def load_keys_fdsn(self, path: str) -> None:
+        """Bootstrapping + key-switch key straight from a reference FDSN BK file."""
+        _lib.check(self.lib.fdsnn_bsk_load_fdsn(self.h, str(path).encode(),
+                                                self.params.digest().encode()))
+        self.keys_loaded = True
+
+    def ciphertexts_fdsn(self, path: str):
+        """(device rows, tensor shape) of a reference FDSN CT file."""
+        cnt = ctypes.c_int64()
+        nd = ctypes.c_int32()
+        shape = (ctypes.c_int64 * 8)()
+        args = (self.h, str(path).encode(), self.params.digest().encode(), ctypes.byref(cnt),
+                ctypes.byref(nd), shape)
+        _lib.check(self.lib.fdsnn_ciphertexts_load_fdsn(*args, None, None))
+        rows = self.empty_rows(int(cnt.value))
+        _lib.check(self.lib.fdsnn_ciphertexts_load_fdsn(*args, _tptr(rows), self._stream()))
+        return rows, tuple(int(shape[i]) for i in range(nd.value))
+
     def lut(self, testpoly: np.ndarray) -> int:
         tp = _i64(testpoly)
         if tp.shape != (self.params.N,):

@@ -225,7 +225,31 @@ def sec_config2():
          boots=np.array([stats.bootstrap_count]), ref_seconds=np.array([dt]), **spikes)
 
 
+def sec_fdsn():
+    """sha256 of FDSN containers written by the reference (TOY keys seed 1)."""
+    import tempfile
+    prm = toy()
+    sk, zk, bsk = W.keys(fdsnn, prm, 1)
+    rng = np.random.default_rng(51)
+    A, b = fdsnn.lwe.encrypt_batch(rng.integers(-3, 5, 12), sk, prm, rng)
+    ct = fdsnn.network.CiphertextTensor((3, 4), A, b, prm.q)
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        paths = {"sk": os.path.join(d, "sk.bin"), "bk": os.path.join(d, "bk.bin"),
+                 "ct": os.path.join(d, "ct.bin")}
+        fdsnn.serial.save_secret_key(paths["sk"], sk, zk, prm)
+        fdsnn.serial.save_bootstrap_key(paths["bk"], bsk)
+        fdsnn.serial.save_ciphertexts(paths["ct"], ct, prm)
+        for k, pth in paths.items():
+            out[k] = fdsnn.serial.file_digest(pth)
+    out["ct_seed"] = 51
+    with open(os.path.join(HERE, "fdsn.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("wrote fdsn.json")
+
+
 SECTIONS = {
+    "fdsn": sec_fdsn,
     "keys": sec_keys, "toy": sec_toy, "toy64": sec_toy64,
     "desk": lambda: sec_lif(W.desk1024(fdsnn), "desk_lif", 32),
     "c4": lambda: sec_lif(W.c4_params(fdsnn), "c4_lif", 4),

@@ -99,3 +99,25 @@ def test_device_rows_roundtrip(desk, desk_keys):
     A2, b2 = dev.rows_to_host(rows)
     assert np.array_equal(A2, A % desk.q) and np.array_equal(b2, b % desk.q)
     assert rows.shape == (17, 516)
+
+
+def test_fdsn_containers_to_device(toy, toy_keys, tmp_path):
+    """Keys and ciphertexts loaded from FDSN files by the C library give the
+    same bootstraps as the in-memory path."""
+    from paper_2309_09025_b200 import serial
+    sk, _, bsk = toy_keys
+    rng = np.random.default_rng(13)
+    ms = rng.integers(-3, 5, 24)
+    A, b = lwe.encrypt_batch(ms, sk, toy, rng)
+    serial.save_bootstrap_key(tmp_path / "bk.bin", bsk)
+    serial.save_ciphertexts(tmp_path / "ct.bin", network.CiphertextTensor((2, 12), A, b, toy.q), toy)
+    dev = serial.load_bootstrap_key_device(tmp_path / "bk.bin", toy)
+    rows, shape = serial.load_ciphertexts_device(tmp_path / "ct.bin", dev)
+    assert shape == (2, 12) and rows.shape[0] == 24
+    g = neuron.g_fire(toy.p)
+    lut = dev.lut(bootstrap.test_polynomial(g, toy))
+    got = dev.rows_to_host(dev.pbs_dev([lut], [0], [0], rows))
+    want = bootstrap.bootstrap_batch(g, A, b, bsk)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    with pytest.raises(errors.ParameterError):
+        serial.load_bootstrap_key_device(tmp_path / "ct.bin", toy)

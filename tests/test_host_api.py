@@ -165,3 +165,29 @@ def test_ciphertext_tensor_checks(toy):
         network.CiphertextTensor((3,), np.zeros((2, toy.n)), np.zeros(2), toy.q)
     z = network.zero_states(5, toy)
     assert z.count == 5 and not np.any(z.A)
+
+
+def test_fdsn_containers_byte_identical_to_reference(toy, toy_keys, tmp_path):
+    """Our FDSN writer produces the reference's exact bytes (sha256 recorded by
+    running the reference's serial.save_* on the same objects)."""
+    from paper_2309_09025_b200 import serial
+    want = json.load(open(os.path.join(GOLDEN, "fdsn.json")))
+    sk, zk, bsk = toy_keys
+    rng = np.random.default_rng(want["ct_seed"])
+    A, b = lwe.encrypt_batch(rng.integers(-3, 5, 12), sk, toy, rng)
+    ct = network.CiphertextTensor((3, 4), A, b, toy.q)
+    serial.save_secret_key(tmp_path / "sk.bin", sk, zk, toy)
+    serial.save_bootstrap_key(tmp_path / "bk.bin", bsk)
+    serial.save_ciphertexts(tmp_path / "ct.bin", ct, toy)
+    for k in ("sk", "bk", "ct"):
+        assert serial.file_digest(tmp_path / f"{k}.bin") == want[k], k
+    sk2, zk2 = serial.load_secret_key(tmp_path / "sk.bin", toy)
+    assert np.array_equal(sk2.s, sk.s) and np.array_equal(zk2.z, zk.z)
+    bk2 = serial.load_bootstrap_key(tmp_path / "bk.bin", toy)
+    assert np.array_equal(bk2.rows, bsk.rows) and np.array_equal(bk2.ksk.A, bsk.ksk.A)
+    ct2 = serial.load_ciphertexts(tmp_path / "ct.bin", toy)
+    assert ct2.shape == (3, 4) and np.array_equal(ct2.A, A) and np.array_equal(ct2.b, b)
+    with pytest.raises(errors.SerializationError):
+        serial.load_ciphertexts(tmp_path / "ct.bin", params.preset("DESK"))
+    with pytest.raises(errors.SerializationError):
+        serial.load_secret_key(tmp_path / "ct.bin", toy)
