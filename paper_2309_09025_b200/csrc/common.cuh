@@ -192,12 +192,6 @@ FDSNN_DEV void tmem_wait16(uint32_t (&w)[16]) {
                  :: "memory");
 }
 // mark registers as completed by an earlier wait (no instruction emitted)
-FDSNN_DEV void tmem_touch16(uint32_t (&w)[16]) {
-    asm volatile(""
-                 : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7]),
-                   "+r"(w[8]), "+r"(w[9]), "+r"(w[10]), "+r"(w[11]), "+r"(w[12]), "+r"(w[13]), "+r"(w[14]), "+r"(w[15])
-                 :: "memory");
-}
 FDSNN_DEV void tmem_touch32(uint32_t (&w)[32]) {
     asm volatile(""
                  : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7]),
@@ -214,18 +208,6 @@ FDSNN_DEV void tmem_st32(uint32_t taddr, const uint32_t (&w)[32]) {
         "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]),
         "r"(w[16]), "r"(w[17]), "r"(w[18]), "r"(w[19]), "r"(w[20]), "r"(w[21]), "r"(w[22]), "r"(w[23]),
         "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]), "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31]) : "memory");
-}
-FDSNN_DEV void put_words_c(uint32_t (&w)[32], int i, double2 c) {
-    w[4 * i] = (uint32_t)__double2loint(c.x);
-    w[4 * i + 1] = (uint32_t)__double2hiint(c.x);
-    w[4 * i + 2] = (uint32_t)__double2loint(c.y);
-    w[4 * i + 3] = (uint32_t)__double2hiint(c.y);
-}
-FDSNN_DEV void tmem_st16w(uint32_t taddr, const uint32_t (&w)[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
-        ::"r"(taddr), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
-        "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]) : "memory");
 }
 FDSNN_DEV double2 words_c(const uint32_t (&w)[32], int i) {
     return make_double2(__hiloint2double((int)w[4 * i + 1], (int)w[4 * i]),

@@ -233,9 +233,7 @@ struct NoHook {
 // `pre_last` runs after the last exchange and twiddle fetch, before the last
 // pass's arithmetic
 // (used to start the key fetch of the following MAC).
-// ONEBUF: buf0 == buf1 (a single exchange buffer) -- each exchange is then
-// also fenced before its stores (write-after-read against the previous one).
-template <int M, bool INV, bool ONEBUF = false, class TW, class HOOK = NoHook>
+template <int M, bool INV, class TW, class HOOK = NoHook>
 FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
                          double2* __restrict__ buf0, double2* __restrict__ buf1,
                          int& ex, const GroupSync& gs, const HOOK& pre_last = HOOK()) {
@@ -249,7 +247,6 @@ FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
         uint32_t raw[32];                                         \
         tw.template issue<PS>(raw);                               \
         double2* b = ex ? buf1 : buf0;                            \
-        if constexpr (ONEBUF) gs.sync();                          \
         pass_store<M, PS - 1>(v, t, b);                           \
         double2 w[8];                                             \
         tw.template finish<PS>(raw, w);                           \
@@ -269,9 +266,7 @@ FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
 // exchanges through buf0, v1 through buf1.  Each exchange is fenced on both
 // sides (write-after-read on the buffers), so it is safe whatever the buffers
 // were last used for.
-// ONEBUF: one exchange buffer (buf0 == buf1): the two transforms exchange one
-// after the other, 4 barriers per exchange instead of 2.
-template <int M, bool INV, bool ONEBUF = false, class TW, class HOOK = NoHook>
+template <int M, bool INV, class TW, class HOOK = NoHook>
 FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& tw,
                           double2* __restrict__ buf0, double2* __restrict__ buf1,
                           const GroupSync& gs, const HOOK& pre_last = HOOK()) {
@@ -287,16 +282,11 @@ FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& t
         tw.template issue<PS>(raw);                               \
         gs.sync();                                                \
         pass_store<M, PS - 1>(v0, t, buf0);                       \
-        if constexpr (!ONEBUF) pass_store<M, PS - 1>(v1, t, buf1); \
+        pass_store<M, PS - 1>(v1, t, buf1);                       \
         double2 w[8];                                             \
         tw.template finish<PS>(raw, w);                           \
         gs.sync();                                                \
         pass_load<M, PS>(v0, t, buf0);                            \
-        if constexpr (ONEBUF) {                                   \
-            gs.sync();                                            \
-            pass_store<M, PS - 1>(v1, t, buf1);                   \
-            gs.sync();                                            \
-        }                                                         \
         pass_load<M, PS>(v1, t, buf1);                            \
         if constexpr (PS == P - 1) pre_last();                    \
         pass_body<M, PS, INV>(v0, w);                             \

@@ -62,8 +62,8 @@ struct PbsShape {
 };
 
 template <int M>
-__host__ __device__ constexpr size_t pbs_group_bytes(int N, int n, bool onebuf = false) {
-    return (onebuf ? 1 : 2) * PbsShape<M>::PADM * sizeof(double2)  // exchange buffers
+__host__ __device__ constexpr size_t pbs_group_bytes(int N, int n) {
+    return 2 * PbsShape<M>::PADM * sizeof(double2)               // exchange buffers
            + 2 * (size_t)N * sizeof(int32_t)                     // accumulator
            + (((size_t)n * sizeof(uint16_t) + 15) & ~(size_t)15);  // a2N
 }
@@ -74,8 +74,8 @@ template <int M>
 __host__ __device__ constexpr size_t pbs_chunk_bytes() { return (size_t)2 * M * sizeof(double2); }
 
 template <int M>
-__host__ __device__ constexpr size_t pbs_smem_bytes(int G, int N, int n, bool onebuf = false) {
-    return 128 + (size_t)PbsRing<M>::S * pbs_chunk_bytes<M>() + (size_t)G * pbs_group_bytes<M>(N, n, onebuf);
+__host__ __device__ constexpr size_t pbs_smem_bytes(int G, int N, int n) {
+    return 128 + (size_t)PbsRing<M>::S * pbs_chunk_bytes<M>() + (size_t)G * pbs_group_bytes<M>(N, n);
 }
 
 template <int M>
@@ -91,20 +91,13 @@ FDSNN_DEV void load_twist(double2 (&tw)[8], int t, const double2* __restrict__ t
 // acc[c][t + rT + h*M] (word 16c + 8h + r): the unrotated operand of
 // (X^k - 1)*ACC and the read half of the accumulator update come from TMEM,
 // so shared memory only serves the rotated reads and the update stores.
-//
-// WIDE variant (16 warps = 8 accumulators per CTA at <= 128 registers): the
-// frequency accumulators O0/O1 of the MAC also live in TMEM between digits,
-// at 256 + 64*(w/4) (4 warp sets per lane quadrant -> all 512 columns), and
-// each accumulator has a single exchange buffer (fft ONEBUF).
 constexpr uint32_t PBS_TMEM_COLS = 256;
 constexpr uint32_t PBS_TMEM_TWIST = 96;
 constexpr uint32_t PBS_TMEM_OWN = 128;
-constexpr uint32_t PBS_TMEM_O = 256;
 
-template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN, bool WIDE = false>
+template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN>
 __global__ void __launch_bounds__(G * (M / 8), 1)
 pbs_blind_rotate_kernel(const PbsArgs args) {
-    constexpr uint32_t TMEM_COLS = WIDE ? 512 : PBS_TMEM_COLS;
     constexpr int T = M / 8;
     constexpr int PADM = PbsShape<M>::PADM;
     constexpr int S = PbsRing<M>::S;
@@ -124,9 +117,9 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     const int warp = threadIdx.x / 32;
     const int g = threadIdx.x / T;
     const int t = threadIdx.x % T;
-    unsigned char* mine = smem_raw + 128 + S * CHUNK + g * pbs_group_bytes<M>(N, n, WIDE);
+    unsigned char* mine = smem_raw + 128 + S * CHUNK + g * pbs_group_bytes<M>(N, n);
     double2* buf0 = reinterpret_cast<double2*>(mine);
-    double2* buf1 = WIDE ? buf0 : buf0 + PADM;
+    double2* buf1 = buf0 + PADM;
     int32_t* acc = reinterpret_cast<int32_t*>(buf1 + PADM);  // [2][N]
     uint16_t* a2N = reinterpret_cast<uint16_t*>(acc + 2 * N);
 
@@ -143,7 +136,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
         }
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc(tmem_base_slot, TMEM_COLS);
+    if (warp == 0) tmem_alloc(tmem_base_slot, PBS_TMEM_COLS);
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
@@ -237,7 +230,6 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
         }
         gs.sync();
         const uint32_t own_col = lane_base + PBS_TMEM_OWN + 32 * (uint32_t)(warp / 4);
-        const uint32_t o_col = lane_base + PBS_TMEM_O + 64 * (uint32_t)(warp / 4);  // WIDE only
         {
             uint32_t w[32];
 #pragma unroll
@@ -253,6 +245,14 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
         const int bg = prm.bg_log;
         const int32_t halfB1 = (1 << (bg - 1)) - 1;  // B/2 - 1
         const int32_t bmask = (1 << bg) - 1;
+        // Signed gadget digits by offset (rgsw.py:130-132 rule): with
+        // y = x + H, H = (B/2-1)(1 + B + ... + B^(l-1)), digit lvl of the centred
+        // x is ((y >> bg*lvl) & (B-1)) - (B/2-1) -- the offset absorbs the
+        // carries, so each level costs a shift, a mask and a subtract.
+        int32_t hsum = 0;
+        for (int lvl = 0; lvl < L; ++lvl) hsum += halfB1 << (bg * lvl);
+        const uint32_t halfq = 1u << (prm.log2q - 1);
+        const int32_t yoff = hsum - (int32_t)halfq;
         int ex = 0;
         double err_max = 0.0;
 
@@ -267,13 +267,15 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                 continue;
             }
             double2 O0[8], O1[8];
-            if constexpr (!WIDE) {
 #pragma unroll
-                for (int r = 0; r < 8; ++r) O0[r] = O1[r] = make_double2(0.0, 0.0);
-            }
+            for (int r = 0; r < 8; ++r) O0[r] = O1[r] = make_double2(0.0, 0.0);
 
-            // centred (X^k - 1)*ACC coefficients {t + rT, t + rT + M} of poly cc
-            auto read_rot = [&](int cc, uint32_t (&rv)[16]) {
+            // rotated reads X^k*ACC at {t + rT, t + rT + M} of poly cc.  Both
+            // polys are read up front: the second set's shared-memory latency
+            // hides behind the first poly's transforms.
+            uint32_t rvs[2][16];
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
                 const int32_t* a = acc + cc * N;
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
@@ -281,177 +283,54 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     for (int half = 0; half < 2; ++half) {
                         const int jj = t + r * T + half * M;
                         const int s = (jj - k) & (2 * N - 1);
-                        rv[8 * half + r] = (s >= N) ? (uint32_t)(-a[s - N]) : (uint32_t)a[s];
+                        rvs[cc][8 * half + r] = (s >= N) ? (uint32_t)(-a[s - N]) : (uint32_t)a[s];
                     }
                 }
-            };
-            auto make_x = [&](int cc, const uint32_t (&rv)[16], int32_t (&xlo)[8], int32_t (&xhi)[8]) {
-                uint32_t ow[16];
-                tmem_ld16_async(own_col + 16 * cc, ow);
-                tmem_wait16(ow);
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    xlo[r] = center_q((rv[r] - ow[r]) & qmask, prm.log2q);
-                    xhi[r] = center_q((rv[8 + r] - ow[8 + r]) & qmask, prm.log2q);
-                }
-            };
-            auto load_x = [&](int cc, int32_t (&xlo)[8], int32_t (&xhi)[8]) {
-                uint32_t ow[16];
-                tmem_ld16_async(own_col + 16 * cc, ow);
-                uint32_t rv[16];
-                read_rot(cc, rv);
-                tmem_wait16(ow);
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    xlo[r] = center_q((rv[r] - ow[r]) & qmask, prm.log2q);
-                    xhi[r] = center_q((rv[8 + r] - ow[8 + r]) & qmask, prm.log2q);
-                }
-            };
-            // next signed gadget digit -> fold, twist, forward transform
-            auto digit_fft = [&](int32_t (&xlo)[8], int32_t (&xhi)[8], double2 (&vv)[8]) {
-                {
-                    uint32_t twr[32];
-                    tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
-                    int32_t d1[8], d2[8];
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        d1[r] = ((xlo[r] + halfB1) & bmask) - halfB1;
-                        d2[r] = ((xhi[r] + halfB1) & bmask) - halfB1;
-                        xlo[r] = (xlo[r] - d1[r]) >> bg;
-                        xhi[r] = (xhi[r] - d2[r]) >> bg;
-                    }
-                    tmem_wait32(twr);
-#pragma unroll
-                    for (int r = 0; r < 8; ++r)
-                        vv[r] = cmul(make_double2((double)d1[r], (double)d2[r]), words_c(twr, r));
-                }
-                fft_group<M, false, WIDE>(vv, t, tw, buf0, buf1, ex, gs);
-            };
-            auto key_chunk = [&](int64_t ch) -> const double2* {
-                const int s = (int)(ch % S);
-                mbar_wait(&full[s], (uint32_t)((ch / S) & 1));
-                return ring + (size_t)s * 2 * M;
-            };
-
-            if constexpr (!WIDE) {
-                // both polys' rotated reads are issued up front: the second set's
-                // shared-memory latency hides behind the first poly's transforms
-                uint32_t rv1[16];
-                read_rot(1, rv1);
-#pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
-                    int32_t xlo[8], xhi[8];
-                    if (cc == 0) {
-                        load_x(0, xlo, xhi);
-                    } else {
-                        make_x(1, rv1, xlo, xhi);
-                    }
-                    for (int lvl = 0; lvl < L; ++lvl, ++c) {
-                        double2 vv[8];
-                        digit_fft(xlo, xhi, vv);
-                        const double2* kd = key_chunk(c);
-#pragma unroll
-                        for (int r = 0; r < 8; ++r) {
-                            cmac(O0[r], vv[r], kd[t + r * T]);
-                            cmac(O1[r], vv[r], kd[M + t + r * T]);
-                        }
-                        release(c);
-                    }
-                }
-            } else {
-                // digits 0 .. 2L-2: frequency accumulators round-trip through TMEM
-                int32_t xlo[8], xhi[8];
-                for (int dg = 0, cc = 0, lvl = 0; dg < 2 * L - 1; ++dg, ++c) {
-                    if (lvl == 0) load_x(cc, xlo, xhi);
-                    double2 vv[8];
-                    digit_fft(xlo, xhi, vv);
-                    const double2* kd = key_chunk(c);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        uint32_t ow[32];
-                        if (dg > 0) {
-                            tmem_ld32_async(o_col + 32 * h, ow);
-                            tmem_wait32(ow);
-                        }
-#pragma unroll
-                        for (int r = 0; r < 8; ++r) {
-                            double2 o = dg > 0 ? words_c(ow, r) : make_double2(0.0, 0.0);
-                            cmac(o, vv[r], kd[h * M + t + r * T]);
-                            put_words_c(ow, r, o);
-                        }
-                        tmem_st32(o_col + 32 * h, ow);
-                    }
-                    tmem_wait_st();
-                    release(c);
-                    if (++lvl == L) { lvl = 0; ++cc; }
-                }
-                // last digit: output 0 comes back into registers, output 1 goes
-                // back to TMEM and is transformed after output 0
-                if (L == 1) load_x(1, xlo, xhi);
-                double2 vv[8];
-                digit_fft(xlo, xhi, vv);
-                const double2* kd = key_chunk(c);
-                {
-                    uint32_t ow[32];
-                    tmem_ld32_async(o_col + 32, ow);
-                    tmem_wait32(ow);
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        double2 o = words_c(ow, r);
-                        cmac(o, vv[r], kd[M + t + r * T]);
-                        put_words_c(ow, r, o);
-                    }
-                    tmem_st32(o_col + 32, ow);
-                }
-                {
-                    uint32_t ow[32];
-                    tmem_ld32_async(o_col, ow);
-                    tmem_wait32(ow);
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        O0[r] = words_c(ow, r);
-                        cmac(O0[r], vv[r], kd[t + r * T]);
-                    }
-                }
-                tmem_wait_st();
-                release(c);
-                ++c;
             }
-            if constexpr (WIDE) {
-#pragma unroll 1
-                for (int cc = 0; cc < 2; ++cc) {
-                    if (cc == 1) {
-                        uint32_t ow[32];
-                        tmem_ld32_async(o_col + 32, ow);
-                        tmem_wait32(ow);
 #pragma unroll
-                        for (int r = 0; r < 8; ++r) O0[r] = words_c(ow, r);
+            for (int cc = 0; cc < 2; ++cc) {
+                int32_t xlo[8], xhi[8];
+                uint32_t ow[16];
+                tmem_ld16_async(own_col + 16 * cc, ow);
+                const uint32_t (&rv)[16] = rvs[cc];
+                tmem_wait16(ow);
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    // y = centred((X^k - 1) ACC) + H
+                    xlo[r] = (int32_t)((rv[r] - ow[r] + halfq) & qmask) + yoff;
+                    xhi[r] = (int32_t)((rv[8 + r] - ow[8 + r] + halfq) & qmask) + yoff;
+                }
+                for (int lvl = 0; lvl < L; ++lvl, ++c) {
+                    double2 vv[8];
+                    {
+                        uint32_t twr[32];
+                        tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
+                        int32_t d1[8], d2[8];
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            d1[r] = (xlo[r] & bmask) - halfB1;
+                            d2[r] = (xhi[r] & bmask) - halfB1;
+                            xlo[r] >>= bg;
+                            xhi[r] >>= bg;
+                        }
+                        tmem_wait32(twr);
+#pragma unroll
+                        for (int r = 0; r < 8; ++r)
+                            vv[r] = cmul(make_double2((double)d1[r], (double)d2[r]), words_c(twr, r));
                     }
-                    fft_group<M, true, true>(O0, t, tw, buf0, buf1, ex, gs);
-                    uint32_t twr[32];
-                    tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
-                    uint32_t own[16];
-                    tmem_ld16_async(own_col + 16 * cc, own);
-                    tmem_wait32(twr);
-                    tmem_touch16(own);
+                    fft_group<M, false>(vv, t, tw, buf0, buf1, ex, gs);
+                    const int s = (int)(c % S);
+                    mbar_wait(&full[s], (uint32_t)((c / S) & 1));
+                    const double2* kd = ring + (size_t)s * 2 * M;
 #pragma unroll
                     for (int r = 0; r < 8; ++r) {
-                        const int p = t + r * T;
-                        const double2 z = cmulc(O0[r], words_c(twr, r));
-                        const long long r0 = round_product(z.x), r1 = round_product(z.y);
-                        if constexpr (TRACK_MARGIN) {
-                            err_max = fmax(err_max, fabs(z.x - (double)r0));
-                            err_max = fmax(err_max, fabs(z.y - (double)r1));
-                        }
-                        own[r] = (own[r] + (uint32_t)r0) & qmask;
-                        own[8 + r] = (own[8 + r] + (uint32_t)r1) & qmask;
-                        acc[cc * N + p] = (int32_t)own[r];
-                        acc[cc * N + p + M] = (int32_t)own[8 + r];
+                        cmac(O0[r], vv[r], kd[t + r * T]);
+                        cmac(O1[r], vv[r], kd[M + t + r * T]);
                     }
-                    tmem_st16w(own_col + 16 * cc, own);
+                    release(c);
                 }
-                tmem_wait_st();
-            } else {
+            }
+            {
                 uint32_t twr[32], own[32];
                 auto fetch = [&]() {
                     tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
@@ -509,7 +388,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     __syncthreads();
     if (warp == 0) {
         tmem_fence_after();
-        tmem_dealloc(tbase, TMEM_COLS);
+        tmem_dealloc(tbase, PBS_TMEM_COLS);
     }
 }
 
