@@ -158,7 +158,7 @@ int fdsnn_sync(fdsnn_ctx* ctx);
 /* Instrumentation used by bench.py / tests.  `which`: 0 = blind rotation,
  * 1 = key switch, 2 = linear operators.  Returns the summed device time (ms)
  * of that kernel family since the last reset, measured with CUDA events on
- * the launching stream, and the launch count. */
+ * the launching stream, and the number of kernels launched. */
 int fdsnn_timing_enable(fdsnn_ctx* ctx, int32_t on);
 int fdsnn_timing_read(fdsnn_ctx* ctx, int32_t which, double* ms, int64_t* launches);
 int fdsnn_timing_reset(fdsnn_ctx* ctx);

@@ -17,6 +17,7 @@
 #include "../../include/fdsnn_b200.h"
 #include "fdsn.h"
 #include "keyswitch.cuh"
+#include "ks_umma.cuh"
 #include "linear.cuh"
 #include "pbs.cuh"
 
@@ -77,6 +78,7 @@ struct Operator {
 struct TimedLaunch {
     int which;
     cudaEvent_t a, b;
+    int kernels;  // kernel launches inside the timed scope
 };
 
 }  // namespace
@@ -89,6 +91,10 @@ struct fdsnn_ctx {
     double2* tables = nullptr;  // W | twist | untw
     double2* bsk = nullptr;
     uint32_t* ksk = nullptr;
+    // tensor-core key switch (ks_umma.cuh): limb tiles of the KSK
+    uint8_t* ks_bt = nullptr;
+    int ks_limbs = 0, ks_ksteps = 0, ks_ntiles = 0;
+    Buf ks_dig;
     bool keys_loaded = false;
     std::vector<int32_t*> luts;
     std::vector<Operator> ops;
@@ -109,6 +115,7 @@ struct TimerScope {
     int which;
     cudaStream_t s;
     cudaEvent_t a = nullptr, b = nullptr;
+    int kernels = 1;
     TimerScope(fdsnn_ctx* c, int w, cudaStream_t st) : ctx(c), which(w), s(st) {
         if (ctx->timing) {
             cudaEventCreate(&a);
@@ -119,7 +126,7 @@ struct TimerScope {
     ~TimerScope() {
         if (ctx->timing) {
             cudaEventRecord(b, s);
-            ctx->timed.push_back({which, a, b});
+            ctx->timed.push_back({which, a, b, kernels});
         }
     }
 };
@@ -166,8 +173,83 @@ int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_
     return set_err(FDSNN_ERR_PARAMETER, "unsupported ring degree N=%d", ctx->dp.N);
 }
 
+unsigned grid1d(int64_t work) {
+    int64_t b = (work + 255) / 256;
+    if (b > 148 * 32) b = 148 * 32;
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}
+
+// Tensor-core key switch applicability: s8 digits, <= 4 byte limbs, exact s32
+// accumulation.  FDSNN_KS_CUDACORE=1 forces the CUDA-core kernels.
+bool ks_umma_ok(const DevParams& d) {
+    const char* e = getenv("FDSNN_KS_CUDACORE");
+    if (e && atoi(e) == 1) return false;
+    const int64_t K = (int64_t)d.N * d.ks_L;
+    return d.ks_log >= 1 && d.ks_log <= 7 && d.log2q <= 32 &&
+           (double)K * (double)(1 << (d.ks_log - 1)) * 255.0 < 2147483647.0;
+}
+
+int prepare_ks_umma(fdsnn_ctx* ctx) {
+    const DevParams& d = ctx->dp;
+    if (!ks_umma_ok(d)) {
+        ctx->ks_limbs = 0;
+        return FDSNN_OK;
+    }
+    const int K = d.N * d.ks_L;
+    const int kq = KSU_KSTEP * KSU_KPS;
+    ctx->ks_limbs = (d.log2q + 7) / 8;
+    ctx->ks_ksteps = ((K + kq - 1) / kq) * KSU_KPS;
+    ctx->ks_ntiles = (d.n + KSU_COLS - 1) / KSU_COLS;
+    const size_t bytes = (size_t)ctx->ks_ntiles * ctx->ks_ksteps * ksu_b_step(ctx->ks_limbs);
+    if (!ctx->ks_bt) CU(cudaMalloc(&ctx->ks_bt, bytes));
+    ksu_prepare_b_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->ksk, K, d.n, d.stride, ctx->ks_ksteps,
+                                                         ctx->ks_limbs, ctx->ks_ntiles, ctx->ks_bt);
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
+template <int KSL>
+int launch_ks_umma_t(fdsnn_ctx* ctx, const KsArgs& a, cudaStream_t s) {
+    const int64_t rblocks = (a.V + KSU_M - 1) / KSU_M;
+    int rc = ctx->ks_dig.ensure((size_t)rblocks * ctx->ks_ksteps * KSU_A_STEP);
+    if (rc) return rc;
+    uint8_t* dig = reinterpret_cast<uint8_t*>(ctx->ks_dig.p);
+    ksu_digits_kernel<KSL><<<grid1d(rblocks * ctx->ks_ksteps * KSU_M * 2), 256, 0, s>>>(a, ctx->ks_ksteps, dig);
+    CU(cudaGetLastError());
+    KsUmmaArgs u{};
+    u.prm = a.prm;
+    u.dig = dig;
+    u.bt = ctx->ks_bt;
+    u.ksteps = ctx->ks_ksteps;
+    u.limbs = ctx->ks_limbs;
+    u.V = a.V;
+    u.out = a.out;
+    dim3 grid((unsigned)rblocks, (unsigned)ctx->ks_ntiles);
+    switch (ctx->ks_limbs) {
+#define FDSNN_KSU(LB)                                                                                  \
+    case LB: {                                                                                         \
+        const size_t smem = ksu_smem_bytes(LB);                                                        \
+        CU(cudaFuncSetAttribute(ks_umma_kernel<LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        ks_umma_kernel<LB><<<grid, 128, smem, s>>>(u);                                                 \
+        break;                                                                                         \
+    }
+        FDSNN_KSU(1)
+        FDSNN_KSU(2)
+        FDSNN_KSU(3)
+        FDSNN_KSU(4)
+#undef FDSNN_KSU
+        default: return set_err(FDSNN_ERR_PARAMETER, "key-switch limbs %d", ctx->ks_limbs);
+    }
+    CU(cudaGetLastError());
+    ks_body_kernel<KSL><<<(unsigned)((a.V + 7) / 8), 256, 0, s>>>(a);
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
 template <int KSL>
 int launch_ks_t(fdsnn_ctx* ctx, const KsArgs& a, cudaStream_t s) {
+    if (ctx->ks_limbs > 0) return launch_ks_umma_t<KSL>(ctx, a, s);
     dim3 grid((unsigned)((a.V + KS_ROWS - 1) / KS_ROWS), (unsigned)((ctx->dp.n + KS_COLS - 1) / KS_COLS));
     ks_mask_kernel<KSL><<<grid, 256, 0, s>>>(a);
     CU(cudaGetLastError());
@@ -179,6 +261,7 @@ int launch_ks_t(fdsnn_ctx* ctx, const KsArgs& a, cudaStream_t s) {
 int launch_ks(fdsnn_ctx* ctx, const KsArgs& a, cudaStream_t s) {
     if (a.V <= 0) return FDSNN_OK;
     TimerScope ts(ctx, 1, s);
+    ts.kernels = ctx->ks_limbs > 0 ? 3 : 2;  // digits + tcgen05 GEMM + body, or mask + body
     switch (ctx->dp.ks_L) {
         case 2: return launch_ks_t<2>(ctx, a, s);
         case 3: return launch_ks_t<3>(ctx, a, s);
@@ -190,12 +273,6 @@ int launch_ks(fdsnn_ctx* ctx, const KsArgs& a, cudaStream_t s) {
     return set_err(FDSNN_ERR_PARAMETER, "unsupported key-switch levels %d", ctx->dp.ks_L);
 }
 
-unsigned grid1d(int64_t work) {
-    int64_t b = (work + 255) / 256;
-    if (b > 148 * 32) b = 148 * 32;
-    if (b < 1) b = 1;
-    return (unsigned)b;
-}
 
 int check_keys(fdsnn_ctx* ctx) {
     if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
@@ -361,6 +438,8 @@ int fdsnn_ctx_destroy(fdsnn_ctx* ctx) {
     cudaFree(ctx->tables);
     cudaFree(ctx->bsk);
     cudaFree(ctx->ksk);
+    cudaFree(ctx->ks_bt);
+    ctx->ks_dig.release();
     cudaFree(ctx->margin);
     ctx->ext.release(); ctx->rows_a.release(); ctx->rows_b.release(); ctx->rows_c.release();
     ctx->host_stage.release(); ctx->acc_buf.release(); ctx->a2n_buf.release(); ctx->l2flush.release();
@@ -413,6 +492,10 @@ int fdsnn_bsk_load(fdsnn_ctx* ctx, const int64_t* rows, const int64_t* ksk_A, co
     }
     if (!ctx->ksk) CU(cudaMalloc(&ctx->ksk, kh.size() * 4));
     CU(cudaMemcpyAsync(ctx->ksk, kh.data(), kh.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    {
+        int rc = prepare_ks_umma(ctx);
+        if (rc) return rc;
+    }
     CU(cudaStreamSynchronize(ctx->stream));
     CU(cudaFree(d_rows));
     ctx->keys_loaded = true;
@@ -763,7 +846,7 @@ int fdsnn_timing_read(fdsnn_ctx* ctx, int32_t which, double* ms, int64_t* launch
         float e = 0.f;
         CU(cudaEventElapsedTime(&e, t.a, t.b));
         ctx->timed_ms[t.which] += e;
-        ctx->timed_n[t.which] += 1;
+        ctx->timed_n[t.which] += t.kernels;
         cudaEventDestroy(t.a);
         cudaEventDestroy(t.b);
     }

@@ -9,6 +9,8 @@
 // int32 GEMMs with wrap-around modulo 2^32, which is exact modulo q = 2^k.
 //
 // Device KSK layout: (N*ks_L) x stride uint32, columns [kskA (n) | kskb | pad].
+// The mask GEMM normally runs on the tensor cores (ks_umma.cuh); the CUDA-core
+// ks_mask_kernel below serves parameter sets outside the int8 bounds.
 #pragma once
 #include "common.cuh"
 
@@ -100,8 +102,8 @@ __global__ void __launch_bounds__(256) ks_mask_kernel(const KsArgs args) {
     }
 }
 
-// Body column: out[v][n] = b' - sum_k dig[v][k] * kskb[k] + out_boff (mod q).
-// One warp per ciphertext.
+// Body column: out[v][n] = b' - sum_k dig[v][k] * kskb[k] + out_boff (mod q),
+// and the row padding (zeros).  One warp per ciphertext.
 template <int KSL>
 __global__ void __launch_bounds__(256) ks_body_kernel(const KsArgs args) {
     const DevParams& prm = args.prm;
@@ -123,6 +125,8 @@ __global__ void __launch_bounds__(256) ks_body_kernel(const KsArgs args) {
     if (lane == 0) {
         const int u = (int)(v / args.count);
         args.out[v * prm.stride + prm.n] = (e[prm.N] - s + args.out_boff[u]) & prm.qmask;
+    } else if (prm.n + lane < prm.stride) {
+        args.out[v * prm.stride + prm.n + lane] = 0u;  // row padding
     }
 }
 

@@ -63,6 +63,32 @@ def test_key_switch_batch(toy, toy_keys):
     assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
 
 
+@pytest.mark.parametrize("which,count", [("toy", 9), ("desk", 130), ("c4prm", 257)])
+def test_key_switch_tensor_core_path(which, count, request, monkeypatch):
+    """The tcgen05 int8 GEMM key switch (4 / 3 byte limbs, ragged 128-row
+    blocks, partial 64-column tiles at n=742) equals the CUDA-core kernels and
+    the oracle bit for bit, including the extreme residues 0 and q-1."""
+    from paper_2309_09025_b200.device import DeviceContext
+    prm = request.getfixturevalue(which)
+    sk, zk, bsk = request.getfixturevalue({"toy": "toy_keys", "desk": "desk_keys", "c4prm": "c4_keys"}[which])
+    rng = np.random.default_rng(17)
+    A = rng.integers(0, prm.q, (count, prm.N))
+    b = rng.integers(0, prm.q, count)
+    A[0] = 0
+    A[1] = prm.q - 1
+    A[2] = prm.q // 2
+    results = []
+    for force in ("0", "1"):
+        monkeypatch.setenv("FDSNN_KS_CUDACORE", force)
+        dev = DeviceContext(prm)
+        dev.load_keys(np.zeros((prm.n, 2 * prm.gadget.levels, 2, prm.N), np.int64), bsk.ksk.A, bsk.ksk.b)
+        results.append(dev.key_switch_batch(A, b))
+        dev.close()
+    want = O.key_switch(A, b, oracle_key(prm, bsk))
+    for got in results:
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
 @pytest.mark.parametrize("which", ["toy64", "desk"])
 def test_lif_step_bit_exact(which, request):
     prm = request.getfixturevalue(which)
