@@ -150,6 +150,19 @@ int fdsnn_operator_apply(fdsnn_ctx* ctx, int32_t op_id, const uint32_t* d_in,
 int fdsnn_rows_add(fdsnn_ctx* ctx, const uint32_t* d_x, const uint32_t* d_y,
                    int64_t count, uint32_t* d_out, void* stream);
 
+/* ---- mod-p plaintext twin (oracle.plain_infer, oracle.py:44-78) ----
+ * int64 device vectors, exact integer arithmetic as in the reference numpy. */
+/* y[b] = M x[b] for a loaded operator (weight layer on plaintext values). */
+int fdsnn_plain_apply(fdsnn_ctx* ctx, int32_t op_id, const int64_t* d_x, int64_t batch,
+                      int64_t* d_y, void* stream);
+/* neuron.plain_lif_step_batch (neuron.py:107-119): h = v + i; spike2 = 2 if
+ * h >= v_th_hat else 0; v' = 0 if fired or h <= 0 else round_half_away(h *
+ * leak_num / leak_den).  p > 0 adds the number of h outside [v_th_hat - p/2,
+ * p/2) to *d_overflow (the reference raises OverflowViolation). */
+int fdsnn_plain_lif(fdsnn_ctx* ctx, const int64_t* d_v, const int64_t* d_i, int64_t count,
+                    int64_t v_th_hat, int64_t leak_num, int64_t leak_den, int64_t p,
+                    int64_t* d_spike2, int64_t* d_v_next, uint64_t* d_overflow, void* stream);
+
 /* Device memory helpers (so a caller without torch can drive the pipeline). */
 int fdsnn_dev_alloc(fdsnn_ctx* ctx, int64_t bytes, void** ptr);
 int fdsnn_dev_free(fdsnn_ctx* ctx, void* ptr);

@@ -289,6 +289,32 @@ def twin_infer(x, layers, T, p):
     return score, spikes_log
 
 
+def plain_infer(x, layers, T, p=None):
+    """oracle.plain_infer (oracle.py:44-78): exact integer forward (no wrap)
+    on the quantized input x.  Returns (scores, per-spiking-layer spike counts
+    summed over T, number of out-of-range charges at p)."""
+    states, counts = {}, {}
+    scores = None
+    overflow = 0
+    for t in range(T):
+        v = np.asarray(x, dtype=np.int64)
+        for li, layer in enumerate(layers):
+            if layer[0] == "weight":
+                v = np.asarray(layer[1], np.int64) @ v
+            else:
+                vth, ln, ld = layer[1:]
+                st = states.get(li, np.zeros(len(v), np.int64))
+                if p is not None:
+                    h = st + v
+                    overflow += int(np.count_nonzero((h < vth - p // 2) | (h >= p // 2)))
+                s, nv = plain_lif_step(st, v, vth, ln, ld)
+                states[li] = nv
+                counts[li] = counts.get(li, 0) + s // 2
+                v = s
+        scores = v if scores is None else scores + v
+    return scores, [counts[k] for k in sorted(counts)], overflow
+
+
 # --------------------------------------------------------- keygen / lwe.py
 
 

@@ -20,6 +20,7 @@
 #include "ks_umma.cuh"
 #include "linear.cuh"
 #include "pbs.cuh"
+#include "plain.cuh"
 
 using namespace fdsnn;
 
@@ -777,6 +778,43 @@ int fdsnn_operator_apply(fdsnn_ctx* ctx, int32_t op_id, const uint32_t* d_in, in
         dim3 grid(op.out_cells, (unsigned)batch);
         linear_csr_kernel<<<grid, 160, 0, s>>>(op.row_ptr, op.col_idx, op.val, op.out_cells, op.in_cells, d_in, d_out, d.stride, d.qmask);
     }
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
+int fdsnn_plain_apply(fdsnn_ctx* ctx, int32_t op_id, const int64_t* d_x, int64_t batch, int64_t* d_y,
+                      void* stream) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    if (op_id < 0 || op_id >= (int32_t)ctx->ops.size()) return set_err(FDSNN_ERR_STATE, "unknown operator %d", op_id);
+    if (batch < 0) return set_err(FDSNN_ERR_PARAMETER, "negative batch");
+    if (batch == 0) return FDSNN_OK;
+    if (!d_x || !d_y) return set_err(FDSNN_ERR_PARAMETER, "null buffer");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t s = pick(ctx, stream);
+    const Operator& op = ctx->ops[op_id];
+    const int64_t warps = batch * op.out_cells;
+    const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
+    if (op.dense)
+        plain_dense_kernel<<<blocks, 256, 0, s>>>(op.w, op.out_cells, op.in_cells, d_x, batch, d_y);
+    else
+        plain_csr_kernel<<<blocks, 256, 0, s>>>(op.row_ptr, op.col_idx, op.val, op.out_cells, op.in_cells, d_x,
+                                                batch, d_y);
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
+int fdsnn_plain_lif(fdsnn_ctx* ctx, const int64_t* d_v, const int64_t* d_i, int64_t count, int64_t v_th_hat,
+                    int64_t leak_num, int64_t leak_den, int64_t p, int64_t* d_spike2, int64_t* d_v_next,
+                    uint64_t* d_overflow, void* stream) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    if (count < 0 || leak_den <= 0 || p < 0) return set_err(FDSNN_ERR_PARAMETER, "bad LIF arguments");
+    if (count == 0) return FDSNN_OK;
+    if (!d_v || !d_i || !d_spike2 || !d_v_next || (p > 0 && !d_overflow))
+        return set_err(FDSNN_ERR_PARAMETER, "null buffer");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t s = pick(ctx, stream);
+    plain_lif_kernel<<<grid1d(count), 256, 0, s>>>(d_v, d_i, count, v_th_hat, leak_num, leak_den, p, d_spike2,
+                                                   d_v_next, reinterpret_cast<unsigned long long*>(d_overflow));
     CU(cudaGetLastError());
     return FDSNN_OK;
 }

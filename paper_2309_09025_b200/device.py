@@ -226,6 +226,27 @@ class DeviceContext:
                                            self._stream()))
         return out
 
+    # ------------------------------------------ mod-p plaintext twin (8(f)1)
+    def plain_apply(self, op_id: int, x, batch: int, out_cells: int):
+        """int64 device vectors: y[b] = M x[b] (oracle.plain_infer weight layer)."""
+        torch = self._torch()
+        y = torch.empty((batch, out_cells), dtype=torch.int64, device=x.device)
+        _lib.check(self.lib.fdsnn_plain_apply(self.h, op_id, _tptr(x), batch, _tptr(y), self._stream()))
+        return y
+
+    def plain_lif(self, v, i, lif, p: int | None, overflow=None):
+        """neuron.plain_lif_step_batch on int64 device tensors -> (spike2, v_next).
+        With p, out-of-range charges are counted into `overflow` (int64[1])."""
+        torch = self._torch()
+        spike2 = torch.empty_like(v)
+        v_next = torch.empty_like(v)
+        _lib.check(self.lib.fdsnn_plain_lif(self.h, _tptr(v), _tptr(i), v.numel(), int(lif.v_th_hat),
+                                            int(lif.leak_num), int(lif.leak_den), int(p or 0),
+                                            _tptr(spike2), _tptr(v_next),
+                                            _tptr(overflow) if overflow is not None else None,
+                                            self._stream()))
+        return spike2, v_next
+
     # ------------------------------------------------------ instrumentation
     def sync(self):
         _lib.check(self.lib.fdsnn_sync(self.h))

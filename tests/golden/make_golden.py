@@ -8,7 +8,7 @@ reference.  Run:
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
         python tests/golden/make_golden.py [section ...]
 
-Sections: keys toy toy64 desk c4 layer config0 config1 config2
+Sections: keys toy toy64 desk c4 layer config0 config1 config2 fdsn plain
 """
 
 from __future__ import annotations
@@ -225,6 +225,37 @@ def sec_config2():
          boots=np.array([stats.bootstrap_count]), ref_seconds=np.array([dt]), **spikes)
 
 
+def sec_plain():
+    """Reference oracle.plain_infer (oracle.py:44-78) on the config 2 network
+    (32 synthetic images, T=4) and the config 4 network (4 images, T=8):
+    integer scores and per-layer spike counts, plus whether the strict range
+    check at p raises."""
+    out = {}
+    for tag, prm, mk, nimg in (("c2", W.desk1024(fdsnn), W.config2_network, 32),
+                               ("c4", W.c4_params(fdsnn), W.config4_network, 4)):
+        lif = W.lif_for(fdsnn, prm)
+        net = mk(fdsnn, lif)
+        imgs = W.synth_images(nimg).astype(np.float64) / 255.0
+        scores, counts = [], None
+        for img in imgs:
+            sc, tr = fdsnn.oracle.plain_infer(net, img)
+            scores.append(sc)
+            c = [np.asarray(s2).sum(axis=0) // 2 for s2 in tr.spike2]
+            counts = [[x] for x in c] if counts is None else [a + [x] for a, x in zip(counts, c)]
+        out[f"{tag}_scores"] = np.stack(scores)
+        for li, c in enumerate(counts):
+            out[f"{tag}_counts{li}"] = np.stack(c)
+        raised = 0
+        for img in imgs:
+            try:
+                fdsnn.oracle.plain_infer(net, img, p=prm.p)
+            except fdsnn.errors.OverflowViolation:
+                raised += 1
+        out[f"{tag}_overflow_images"] = np.array([raised])
+        print(tag, "scores", out[f"{tag}_scores"][0], "overflowing images at p:", raised)
+    save("plain", **out)
+
+
 def sec_fdsn():
     """sha256 of FDSN containers written by the reference (TOY keys seed 1)."""
     import tempfile
@@ -254,6 +285,7 @@ SECTIONS = {
     "desk": lambda: sec_lif(W.desk1024(fdsnn), "desk_lif", 32),
     "c4": lambda: sec_lif(W.c4_params(fdsnn), "c4_lif", 4),
     "layer": sec_layer, "config0": sec_config0, "config1": sec_config1, "config2": sec_config2,
+    "plain": sec_plain,
 }
 
 if __name__ == "__main__":

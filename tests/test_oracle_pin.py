@@ -151,3 +151,33 @@ def test_oracle_compiled_path_matches(toy64, toy64_keys):
     a = O.lif_step_fast(g["vA"], g["vb"], g["iA"], g["ib"], 10, 1, 2, key)
     for x, nm in zip(a, ("sA", "sb", "nA", "nb")):
         assert np.array_equal(x, g[nm])
+
+
+def _plain_case(tag, prm):
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import workloads as W
+    import paper_2309_09025_b200 as api
+    lif = W.lif_for(api, prm)
+    net = (W.config2_network if tag == "c2" else W.config4_network)(api, lif)
+    nimg = 32 if tag == "c2" else 4
+    imgs = W.synth_images(nimg)
+    return net, imgs, W.layers_for_oracle(net)
+
+
+@pytest.mark.parametrize("tag", ["c2", "c4"])
+def test_oracle_plain_infer_golden(tag, desk, c4prm):
+    """oracle.plain_infer restatement == the reference's plain_infer (scores,
+    per-layer spike counts, range-check failures at p) on configs 2 and 4."""
+    g = load("plain")
+    prm = desk if tag == "c2" else c4prm
+    net, imgs, layers = _plain_case(tag, prm)
+    overflowing = 0
+    for k, img in enumerate(imgs):
+        x = (img.astype(np.float64) / 255.0 >= 0.5).astype(np.int64).ravel()
+        sc, counts, over = O.plain_infer(x, layers, net.T, prm.p)
+        assert np.array_equal(sc, g[f"{tag}_scores"][k]), k
+        for li, c in enumerate(counts):
+            assert np.array_equal(c, g[f"{tag}_counts{li}"][k]), (k, li)
+        overflowing += over > 0
+    assert overflowing == int(g[f"{tag}_overflow_images"][0])
