@@ -150,6 +150,19 @@ int fdsnn_operator_apply(fdsnn_ctx* ctx, int32_t op_id, const uint32_t* d_in,
 int fdsnn_rows_add(fdsnn_ctx* ctx, const uint32_t* d_x, const uint32_t* d_y,
                    int64_t count, uint32_t* d_out, void* stream);
 
+/* ---- client-side encryption on the device -------------
+ * The randomness is drawn by the caller in the reference's order (masks A on
+ * the q/2N grid, rounded-Gaussian e: lwe.encrypt_batch, lwe.py:75-87); the
+ * device computes b = <A, s> + e + Delta*m mod q into rows.  sk is the host
+ * binary secret (n int64), A (count, n), e and m (count,) host int64.
+ * Messages outside {-p/2+1..p/2} -> FDSNN_ERR_DOMAIN. */
+int fdsnn_encrypt_rows(fdsnn_ctx* ctx, const int64_t* sk, const int64_t* A, const int64_t* e,
+                       const int64_t* m, int64_t count, uint32_t* d_rows, void* stream);
+/* lwe.decrypt_batch (lwe.py:89-96) of device rows into host m (count int64);
+ * returns when m is on the host. */
+int fdsnn_decrypt_rows(fdsnn_ctx* ctx, const int64_t* sk, const uint32_t* d_rows, int64_t count,
+                       int64_t* m, void* stream);
+
 /* ---- mod-p plaintext twin (oracle.plain_infer, oracle.py:44-78) ----
  * int64 device vectors, exact integer arithmetic as in the reference numpy. */
 /* y[b] = M x[b] for a loaded operator (weight layer on plaintext values). */

@@ -60,6 +60,8 @@ SIGNATURES = {
     "fdsnn_operator_apply": (_c_int, [_vp, _i32, _vp, _i64, _vp, _vp]),
     "fdsnn_rows_add": (_c_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "fdsnn_plain_apply": (_c_int, [_vp, _i32, _vp, _i64, _vp, _vp]),
+    "fdsnn_encrypt_rows": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "fdsnn_decrypt_rows": (_c_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "fdsnn_plain_lif": (_c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
     "fdsnn_dev_alloc": (_c_int, [_vp, _i64, ctypes.POINTER(_vp)]),
     "fdsnn_dev_free": (_c_int, [_vp, _vp]),

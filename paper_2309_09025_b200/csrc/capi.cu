@@ -21,6 +21,7 @@
 #include "linear.cuh"
 #include "pbs.cuh"
 #include "plain.cuh"
+#include "lwe_dev.cuh"
 
 using namespace fdsnn;
 
@@ -580,6 +581,71 @@ int fdsnn_rows_from_host(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b, int
     CU(cudaMemcpyAsync(db, b, bbytes, cudaMemcpyHostToDevice, s));
     rows_pack_kernel<<<grid1d(count * d.stride), 256, 0, s>>>(dA, db, count, d.n, d.stride, d.qmask, d_rows);
     CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
+// Stage the binary secret key s (n values) as int32 on the device.
+int stage_secret(fdsnn_ctx* ctx, const int64_t* s, int32_t* dst, cudaStream_t st) {
+    const DevParams& d = ctx->dp;
+    std::vector<int32_t> h((size_t)d.n);
+    for (int i = 0; i < d.n; ++i) {
+        if (s[i] != 0 && s[i] != 1) return set_err(FDSNN_ERR_DOMAIN, "secret key entries must be 0/1");
+        h[i] = (int32_t)s[i];
+    }
+    CU(cudaMemcpyAsync(dst, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st));
+    return FDSNN_OK;
+}
+
+int fdsnn_encrypt_rows(fdsnn_ctx* ctx, const int64_t* sk, const int64_t* A, const int64_t* e,
+                       const int64_t* m, int64_t count, uint32_t* d_rows, void* stream) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    if (count < 0) return set_err(FDSNN_ERR_PARAMETER, "negative count");
+    if (count == 0) return FDSNN_OK;
+    if (!sk || !A || !e || !m || !d_rows) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+    const DevParams& d = ctx->dp;
+    for (int64_t i = 0; i < count; ++i)
+        if (m[i] < -d.p / 2 + 1 || m[i] > d.p / 2) return set_err(FDSNN_ERR_DOMAIN, "message outside centered Z_p");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t st = pick(ctx, stream);
+    const size_t abytes = (size_t)count * d.n * 8, bbytes = (size_t)count * 8;
+    int rc;
+    if ((rc = ctx->host_stage.ensure(abytes + 2 * bbytes + (size_t)d.n * 4 + 16))) return rc;
+    int64_t* dA = (int64_t*)ctx->host_stage.p;
+    int64_t* de = dA + (size_t)count * d.n;
+    int64_t* dm = de + count;
+    int32_t* ds = reinterpret_cast<int32_t*>(dm + count);
+    CU(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(de, e, bbytes, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(dm, m, bbytes, cudaMemcpyHostToDevice, st));
+    if ((rc = stage_secret(ctx, sk, ds, st))) return rc;
+    rows_pack_kernel<<<grid1d(count * d.stride), 256, 0, st>>>(dA, de, count, d.n, d.stride, d.qmask, d_rows);
+    CU(cudaGetLastError());
+    const uint32_t delta = (uint32_t)((1ll << d.log2q) / d.p);
+    lwe_encrypt_kernel<<<(unsigned)((count * 32 + 255) / 256), 256, 0, st>>>(d_rows, count, d.stride, d.n, ds, de,
+                                                                           dm, d.qmask, delta);
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
+int fdsnn_decrypt_rows(fdsnn_ctx* ctx, const int64_t* sk, const uint32_t* d_rows, int64_t count, int64_t* m,
+                       void* stream) {
+    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+    if (count < 0) return set_err(FDSNN_ERR_PARAMETER, "negative count");
+    if (count == 0) return FDSNN_OK;
+    if (!sk || !d_rows || !m) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+    const DevParams& d = ctx->dp;
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t st = pick(ctx, stream);
+    int rc;
+    if ((rc = ctx->host_stage.ensure((size_t)count * 8 + (size_t)d.n * 4 + 16))) return rc;
+    int64_t* dout = (int64_t*)ctx->host_stage.p;
+    int32_t* ds = reinterpret_cast<int32_t*>(dout + count);
+    if ((rc = stage_secret(ctx, sk, ds, st))) return rc;
+    lwe_decrypt_kernel<<<(unsigned)((count * 32 + 255) / 256), 256, 0, st>>>(d_rows, count, d.stride, d.n, ds,
+                                                                           d.log2q, d.p, dout);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(m, dout, (size_t)count * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
     return FDSNN_OK;
 }
 

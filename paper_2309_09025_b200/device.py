@@ -15,7 +15,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .errors import DeviceError, ParameterError
+from .errors import DeviceError, DomainError, ParameterError
 from .params import FheParams
 
 
@@ -224,6 +224,32 @@ class DeviceContext:
             out = self.empty_rows(x.shape[0])
         _lib.check(self.lib.fdsnn_rows_add(self.h, _tptr(x), _tptr(y), x.shape[0], _tptr(out),
                                            self._stream()))
+        return out
+
+    # ------------------------------------------- client side on device (8(f)4)
+    def encrypt_rows(self, ms, sk, rng, sigma=None):
+        """lwe.encrypt_batch with the device computing b = <A,s> + e + Delta*m.
+        A and e are drawn from `rng` exactly as the reference draws them, so the
+        rows equal the reference's (A, b) for the same generator state."""
+        from .lwe import sample_noise
+        p = self.params
+        ms = _i64(np.asarray(ms).ravel())
+        if np.any(ms < -p.p // 2 + 1) or np.any(ms > p.p // 2):
+            raise DomainError("message outside centered Z_p")  # before any draw, as lwe.py:79-80
+        grid = p.grid
+        A = _i64(rng.integers(0, p.q // grid, size=(ms.size, p.n)) * grid)
+        sig = p.sigma if sigma is None else sigma
+        e = _i64(sample_noise(rng, sig, ms.size) if sig > 0 else np.zeros(ms.size, dtype=np.int64))
+        rows = self.empty_rows(ms.size)
+        _lib.check(self.lib.fdsnn_encrypt_rows(self.h, _ptr(_i64(sk.s)), _ptr(A), _ptr(e), _ptr(ms), ms.size,
+                                               _tptr(rows), self._stream()))
+        return rows
+
+    def decrypt_rows(self, rows, sk) -> np.ndarray:
+        """lwe.decrypt_batch of device rows (lwe.py:89-96)."""
+        out = np.empty(rows.shape[0], dtype=np.int64)
+        _lib.check(self.lib.fdsnn_decrypt_rows(self.h, _ptr(_i64(sk.s)), _tptr(rows), rows.shape[0], _ptr(out),
+                                               self._stream()))
         return out
 
     # ------------------------------------------ mod-p plaintext twin (8(f)1)
