@@ -140,10 +140,10 @@ cudaStream_t pick(fdsnn_ctx* ctx, void* stream) {
     return stream ? reinterpret_cast<cudaStream_t>(stream) : cudaStreamLegacy;
 }
 
-template <int M, int G, bool RAW, bool MARGIN>
+template <int M, int G, bool RAW, bool MARGIN, bool PAIR>
 int launch_br_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_t s) {
     const size_t smem = pbs_smem_bytes<M>(G, 2 * M, ctx->dp.n);
-    auto kern = pbs_blind_rotate_kernel<M, G, RAW, MARGIN>;
+    auto kern = pbs_blind_rotate_kernel<M, G, RAW, MARGIN, PAIR>;
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (V + G - 1) / G;
     kern<<<(unsigned)blocks, G * (M / 8), smem, s>>>(a);
@@ -151,12 +151,12 @@ int launch_br_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_t s) {
     return FDSNN_OK;
 }
 
-template <int M, int G>
+template <int M, int G, bool PAIR = false>
 int launch_br_m(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_t s) {
-    if (raw) return ctx->track_margin ? launch_br_t<M, G, true, true>(ctx, a, V, s)
-                                      : launch_br_t<M, G, true, false>(ctx, a, V, s);
-    return ctx->track_margin ? launch_br_t<M, G, false, true>(ctx, a, V, s)
-                             : launch_br_t<M, G, false, false>(ctx, a, V, s);
+    if (raw) return ctx->track_margin ? launch_br_t<M, G, true, true, PAIR>(ctx, a, V, s)
+                                      : launch_br_t<M, G, true, false, PAIR>(ctx, a, V, s);
+    return ctx->track_margin ? launch_br_t<M, G, false, true, PAIR>(ctx, a, V, s)
+                             : launch_br_t<M, G, false, false, PAIR>(ctx, a, V, s);
 }
 
 int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_t s) {
@@ -168,6 +168,11 @@ int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_
             // accumulators per CTA: 4 amortises each key chunk over 4 rotations;
             // small batches spread over more SMs instead (latency-bound regime)
             // (G=1 CTAs are small enough for 2 per SM: <= 296 rotations fit in one wave)
+            // gadget levels L == 2 (DESK): the paired-level transform variant
+            if (ctx->dp.L == 2) {
+                if (V > 2 * 148) return launch_br_m<512, 4, true>(ctx, a, V, raw, s);
+                return launch_br_m<512, 1, true>(ctx, a, V, raw, s);
+            }
             if (V > 2 * 148) return launch_br_m<512, 4>(ctx, a, V, raw, s);
             return launch_br_m<512, 1>(ctx, a, V, raw, s);
         case 1024: return launch_br_m<1024, 2>(ctx, a, V, raw, s);

@@ -209,6 +209,12 @@ FDSNN_DEV void tmem_st32(uint32_t taddr, const uint32_t (&w)[32]) {
         "r"(w[16]), "r"(w[17]), "r"(w[18]), "r"(w[19]), "r"(w[20]), "r"(w[21]), "r"(w[22]), "r"(w[23]),
         "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]), "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31]) : "memory");
 }
+FDSNN_DEV void put_words_c(uint32_t (&w)[32], int i, double2 c) {
+    w[4 * i] = (uint32_t)__double2loint(c.x);
+    w[4 * i + 1] = (uint32_t)__double2hiint(c.x);
+    w[4 * i + 2] = (uint32_t)__double2loint(c.y);
+    w[4 * i + 3] = (uint32_t)__double2hiint(c.y);
+}
 FDSNN_DEV double2 words_c(const uint32_t (&w)[32], int i) {
     return make_double2(__hiloint2double((int)w[4 * i + 1], (int)w[4 * i]),
                         __hiloint2double((int)w[4 * i + 3], (int)w[4 * i + 2]));

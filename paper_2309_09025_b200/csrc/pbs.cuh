@@ -95,9 +95,15 @@ constexpr uint32_t PBS_TMEM_COLS = 256;
 constexpr uint32_t PBS_TMEM_TWIST = 96;
 constexpr uint32_t PBS_TMEM_OWN = 128;
 
-template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN>
+// PAIR (gadget levels L == 2): the two levels of a polynomial are transformed
+// together (fft_group2: two independent transforms per thread, one barrier
+// pair per exchange) and MAC'd together; the first polynomial's partial
+// frequency accumulators wait in TMEM (columns 256 + 64*(w/4)) while the
+// second polynomial is transformed.
+template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN, bool PAIR = false>
 __global__ void __launch_bounds__(G * (M / 8), 1)
 pbs_blind_rotate_kernel(const PbsArgs args) {
+    constexpr uint32_t TMEM_COLS = PAIR ? 512 : PBS_TMEM_COLS;
     constexpr int T = M / 8;
     constexpr int PADM = PbsShape<M>::PADM;
     constexpr int S = PbsRing<M>::S;
@@ -136,7 +142,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
         }
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc(tmem_base_slot, PBS_TMEM_COLS);
+    if (warp == 0) tmem_alloc(tmem_base_slot, TMEM_COLS);
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
@@ -230,6 +236,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
         }
         gs.sync();
         const uint32_t own_col = lane_base + PBS_TMEM_OWN + 32 * (uint32_t)(warp / 4);
+        const uint32_t o_col = lane_base + 256 + 64 * (uint32_t)(warp / 4);  // PAIR only
         {
             uint32_t w[32];
 #pragma unroll
@@ -267,8 +274,10 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                 continue;
             }
             double2 O0[8], O1[8];
+            if constexpr (!PAIR) {
 #pragma unroll
-            for (int r = 0; r < 8; ++r) O0[r] = O1[r] = make_double2(0.0, 0.0);
+                for (int r = 0; r < 8; ++r) O0[r] = O1[r] = make_double2(0.0, 0.0);
+            }
 
             // rotated reads X^k*ACC at {t + rT, t + rT + M} of poly cc.  Both
             // polys are read up front: the second set's shared-memory latency
@@ -300,6 +309,66 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     xlo[r] = (int32_t)((rv[r] - ow[r] + halfq) & qmask) + yoff;
                     xhi[r] = (int32_t)((rv[8 + r] - ow[8 + r] + halfq) & qmask) + yoff;
                 }
+                if constexpr (PAIR) {
+                    double2 v0[8], v1[8];
+                    {
+                        uint32_t twr[32];
+                        tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
+                        int32_t d1[8], d2[8], e1[8], e2[8];
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            d1[r] = (xlo[r] & bmask) - halfB1;
+                            d2[r] = (xhi[r] & bmask) - halfB1;
+                            e1[r] = ((xlo[r] >> bg) & bmask) - halfB1;
+                            e2[r] = ((xhi[r] >> bg) & bmask) - halfB1;
+                        }
+                        tmem_wait32(twr);
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            const double2 tr = words_c(twr, r);
+                            v0[r] = cmul(make_double2((double)d1[r], (double)d2[r]), tr);
+                            v1[r] = cmul(make_double2((double)e1[r], (double)e2[r]), tr);
+                        }
+                    }
+                    fft_group2<M, false>(v0, v1, t, tw, buf0, buf1, gs);
+                    const int s0 = (int)(c % S), s1 = (int)((c + 1) % S);
+                    mbar_wait(&full[s0], (uint32_t)((c / S) & 1));
+                    mbar_wait(&full[s1], (uint32_t)(((c + 1) / S) & 1));
+                    const double2* k0 = ring + (size_t)s0 * 2 * M;
+                    const double2* k1 = ring + (size_t)s1 * 2 * M;
+                    if (cc == 0) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            uint32_t ow2[32];
+#pragma unroll
+                            for (int r = 0; r < 8; ++r) {
+                                double2 o = make_double2(0.0, 0.0);
+                                cmac(o, v0[r], k0[h * M + t + r * T]);
+                                cmac(o, v1[r], k1[h * M + t + r * T]);
+                                put_words_c(ow2, r, o);
+                            }
+                            tmem_st32(o_col + 32 * h, ow2);
+                        }
+                        tmem_wait_st();
+                    } else {
+                        uint32_t oa[32], ob[32];
+                        tmem_ld32_async(o_col, oa);
+                        tmem_ld32_async(o_col + 32, ob);
+                        tmem_wait64(oa, ob);
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            O0[r] = words_c(oa, r);
+                            O1[r] = words_c(ob, r);
+                            cmac(O0[r], v0[r], k0[t + r * T]);
+                            cmac(O1[r], v0[r], k0[M + t + r * T]);
+                            cmac(O0[r], v1[r], k1[t + r * T]);
+                            cmac(O1[r], v1[r], k1[M + t + r * T]);
+                        }
+                    }
+                    release(c);
+                    release(c + 1);
+                    c += 2;
+                } else
                 for (int lvl = 0; lvl < L; ++lvl, ++c) {
                     double2 vv[8];
                     {
@@ -388,7 +457,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     __syncthreads();
     if (warp == 0) {
         tmem_fence_after();
-        tmem_dealloc(tbase, PBS_TMEM_COLS);
+        tmem_dealloc(tbase, TMEM_COLS);
     }
 }
 
