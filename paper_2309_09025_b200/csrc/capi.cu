@@ -96,7 +96,10 @@ struct fdsnn_ctx {
     // tensor-core key switch (ks_umma.cuh): limb tiles of the KSK
     uint8_t* ks_bt = nullptr;
     int ks_limbs = 0, ks_ksteps = 0, ks_ntiles = 0;
-    Buf ks_dig;
+    // Per-stream scratch of the PBS pipeline (extracted z-LWE rows, key-switch
+    // digit tiles), so launches on different streams never share buffers.
+    struct StreamScratch { Buf ext, ks_dig; };
+    std::map<cudaStream_t, StreamScratch> scratch;
     bool keys_loaded = false;
     std::vector<int32_t*> luts;
     std::vector<Operator> ops;
@@ -219,9 +222,10 @@ int prepare_ks_umma(fdsnn_ctx* ctx) {
 template <int KSL>
 int launch_ks_umma_t(fdsnn_ctx* ctx, const KsArgs& a, cudaStream_t s) {
     const int64_t rblocks = (a.V + KSU_M - 1) / KSU_M;
-    int rc = ctx->ks_dig.ensure((size_t)rblocks * ctx->ks_ksteps * KSU_A_STEP);
+    Buf& digbuf = ctx->scratch[s].ks_dig;
+    int rc = digbuf.ensure((size_t)rblocks * ctx->ks_ksteps * KSU_A_STEP);
     if (rc) return rc;
-    uint8_t* dig = reinterpret_cast<uint8_t*>(ctx->ks_dig.p);
+    uint8_t* dig = reinterpret_cast<uint8_t*>(digbuf.p);
     ksu_digits_kernel<KSL><<<grid1d(rblocks * ctx->ks_ksteps * KSU_M * 2), 256, 0, s>>>(a, ctx->ks_ksteps, dig);
     CU(cudaGetLastError());
     KsUmmaArgs u{};
@@ -321,13 +325,14 @@ int pbs_pipeline(fdsnn_ctx* ctx, int nlut, const int32_t* lut_ids, const int64_t
     a.bsk = ctx->bsk;
     a.tables = ctx->tables;
     const int64_t V = count * nlut;
-    if ((rc = ctx->ext.ensure((size_t)V * ctx->dp.ext_stride * 4))) return rc;
-    a.ext_out = (uint32_t*)ctx->ext.p;
+    Buf& ext = ctx->scratch[s].ext;
+    if ((rc = ext.ensure((size_t)V * ctx->dp.ext_stride * 4))) return rc;
+    a.ext_out = (uint32_t*)ext.p;
     a.margin = ctx->margin;
     if ((rc = launch_br(ctx, a, V, false, s))) return rc;
     KsArgs k{};
     k.prm = ctx->dp;
-    k.ext = (const uint32_t*)ctx->ext.p;
+    k.ext = (const uint32_t*)ext.p;
     k.V = V;
     k.ksk = ctx->ksk;
     k.out = d_out;
@@ -446,7 +451,7 @@ int fdsnn_ctx_destroy(fdsnn_ctx* ctx) {
     cudaFree(ctx->bsk);
     cudaFree(ctx->ksk);
     cudaFree(ctx->ks_bt);
-    ctx->ks_dig.release();
+    for (auto& kv : ctx->scratch) { kv.second.ext.release(); kv.second.ks_dig.release(); }
     cudaFree(ctx->margin);
     ctx->ext.release(); ctx->rows_a.release(); ctx->rows_b.release(); ctx->rows_c.release();
     ctx->host_stage.release(); ctx->acc_buf.release(); ctx->a2n_buf.release(); ctx->l2flush.release();
