@@ -6,16 +6,16 @@ import torch
 from paper_2309_09025_b200 import bootstrap, lwe, neuron, params, rgsw
 from paper_2309_09025_b200.bootstrap import test_polynomial
 
-prm = params.preset("DESK").with_p(1024)
+prm = params.c4() if os.environ.get("PROBE_PARAMS") == "c4" else params.preset("DESK").with_p(1024)
 rng = np.random.default_rng(0)
 sk = lwe.lwe_keygen(prm, rng); zk = rgsw.rlwe_keygen(prm, rng)
 t = time.time(); bsk = bootstrap.gen_bootstrap_key(sk, zk, prm, rng); print("keygen s", time.time() - t)
 dev = bsk.device
 print("fp64 peak TF", dev.fp64_peak_tflops())
-lif = neuron.LifParams(tau=2, theta=64)
+lif = neuron.LifParams(tau=2, theta=256 if prm.p == 4096 else 64)
 lf = dev.lut(test_polynomial(neuron.g_fire(prm.p), prm)); lr = dev.lut(test_polynomial(neuron.g_reset(lif, prm.p), prm))
 for B in (int(x) for x in sys.argv[1:] or ["4096"]):
-    ms = rng.integers(-511, 513, B)
+    ms = rng.integers(-prm.p // 2 + 1, prm.p // 2 + 1, B)
     A, b = lwe.encrypt_batch(ms, sk, prm, rng)
     rows = dev.rows_from_host(A, b)
     zero = dev.zero_rows(B)
