@@ -93,6 +93,7 @@ struct fdsnn_ctx {
     double2* tables = nullptr;  // W | twist | untw
     double2* bsk = nullptr;
     uint32_t* ksk = nullptr;
+    uint32_t* kskb = nullptr;  // body column of the KSK, contiguous
     // tensor-core key switch (ks_umma.cuh): limb tiles of the KSK
     uint8_t* ks_bt = nullptr;
     int ks_limbs = 0, ks_ksteps = 0, ks_ntiles = 0;
@@ -335,6 +336,7 @@ int pbs_pipeline(fdsnn_ctx* ctx, int nlut, const int32_t* lut_ids, const int64_t
     k.ext = (const uint32_t*)ext.p;
     k.V = V;
     k.ksk = ctx->ksk;
+    k.kskb = ctx->kskb;
     k.out = d_out;
     k.count = count;
     for (int u = 0; u < nlut; ++u) k.out_boff[u] = out_boff ? delta_times(ctx, out_boff[u]) : 0u;
@@ -450,6 +452,7 @@ int fdsnn_ctx_destroy(fdsnn_ctx* ctx) {
     cudaFree(ctx->tables);
     cudaFree(ctx->bsk);
     cudaFree(ctx->ksk);
+    cudaFree(ctx->kskb);
     cudaFree(ctx->ks_bt);
     for (auto& kv : ctx->scratch) { kv.second.ext.release(); kv.second.ks_dig.release(); }
     cudaFree(ctx->margin);
@@ -504,6 +507,10 @@ int fdsnn_bsk_load(fdsnn_ctx* ctx, const int64_t* rows, const int64_t* ksk_A, co
     }
     if (!ctx->ksk) CU(cudaMalloc(&ctx->ksk, kh.size() * 4));
     CU(cudaMemcpyAsync(ctx->ksk, kh.data(), kh.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<uint32_t> kb((size_t)krows);
+    for (int64_t r = 0; r < krows; ++r) kb[r] = kh[r * d.stride + d.n];
+    if (!ctx->kskb) CU(cudaMalloc(&ctx->kskb, kb.size() * 4));
+    CU(cudaMemcpyAsync(ctx->kskb, kb.data(), kb.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
     {
         int rc = prepare_ks_umma(ctx);
         if (rc) return rc;
@@ -780,6 +787,7 @@ int fdsnn_key_switch_batch(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b, i
     k.ext = (const uint32_t*)ctx->ext.p;
     k.V = count;
     k.ksk = ctx->ksk;
+    k.kskb = ctx->kskb;
     k.out = (uint32_t*)ctx->rows_b.p;
     k.count = count;
     if ((rc = launch_ks(ctx, k, ctx->stream))) return rc;

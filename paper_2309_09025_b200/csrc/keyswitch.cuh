@@ -25,6 +25,7 @@ struct KsArgs {
     const uint32_t* ext;   // V x ext_stride (z-LWE rows, a'_0..a'_{N-1}, b')
     int64_t V;
     const uint32_t* ksk;   // (N*ks_L) x stride
+    const uint32_t* kskb;  // (N*ks_L) body column, contiguous (coalesced reads)
     uint32_t* out;         // V x stride
     int64_t count;         // rows per LUT (for out_boff selection)
     uint32_t out_boff[4];  // added to the output body, per LUT (mod q)
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(256) ks_body_kernel(const KsArgs args) {
 #pragma unroll
         for (int lv = 0; lv < KSL; ++lv) {
             const int32_t d = ks_digit(x, prm.ks_log);
-            s += (uint32_t)d * __ldg(args.ksk + (size_t)(j * KSL + lv) * prm.stride + prm.n);
+            s += (uint32_t)d * __ldg(args.kskb + j * KSL + lv);
         }
     }
 #pragma unroll
