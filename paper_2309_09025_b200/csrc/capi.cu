@@ -101,6 +101,7 @@ struct fdsnn_ctx {
     // digit tiles), so launches on different streams never share buffers.
     struct StreamScratch { Buf ext, ks_dig; };
     std::map<cudaStream_t, StreamScratch> scratch;
+    int64_t wide_max = 148;  // largest batch routed to the latency kernel (FDSNN_WIDE_MAX)
     bool keys_loaded = false;
     std::vector<int32_t*> luts;
     std::vector<Operator> ops;
@@ -163,6 +164,16 @@ int launch_br_m(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStrea
                              : launch_br_t<M, G, false, false, PAIR>(ctx, a, V, s);
 }
 
+template <bool RAW, bool MARGIN>
+int launch_br_wide_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_t s) {
+    const size_t smem = pbs_wide_smem_bytes<512>(4, 1024, ctx->dp.n);
+    auto kern = pbs_blind_rotate_wide_kernel<512, RAW, MARGIN, 4>;
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)V, 4 * 64, smem, s>>>(a);
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
 int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_t s) {
     if (V <= 0) return FDSNN_OK;
     TimerScope ts(ctx, 0, s);
@@ -174,6 +185,12 @@ int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_
             // (G=1 CTAs are small enough for 2 per SM: <= 296 rotations fit in one wave)
             // gadget levels L == 2 (DESK): the paired-level transform variant
             if (ctx->dp.L == 2) {
+                if (V <= ctx->wide_max) {  // latency regime: one CTA per rotation, digits in parallel
+                    if (raw) return ctx->track_margin ? launch_br_wide_t<true, true>(ctx, a, V, s)
+                                                      : launch_br_wide_t<true, false>(ctx, a, V, s);
+                    return ctx->track_margin ? launch_br_wide_t<false, true>(ctx, a, V, s)
+                                             : launch_br_wide_t<false, false>(ctx, a, V, s);
+                }
                 if (V > 2 * 148) return launch_br_m<512, 4, true>(ctx, a, V, raw, s);
                 return launch_br_m<512, 1, true>(ctx, a, V, raw, s);
             }
@@ -389,6 +406,8 @@ int fdsnn_ctx_create(const fdsnn_params* prm, int32_t device, fdsnn_ctx** out) {
     fdsnn_ctx* ctx = new fdsnn_ctx();
     ctx->prm = p;
     ctx->device = device;
+    ctx->wide_max = dprop.multiProcessorCount;
+    if (const char* e = getenv("FDSNN_WIDE_MAX")) ctx->wide_max = atoll(e);
     DevParams& d = ctx->dp;
     d.n = p.n;
     d.N = p.N;

@@ -461,6 +461,262 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Latency variant for small batches (fewer rotations than SMs): one CTA per
+// accumulator, 2L warp-pairs (256 threads at l = 2), so the 2L forward
+// transforms of a CMux step run in parallel instead of one after another.
+// Warp-pair p transforms digit p = (poly cc = p / L, level p % L) and multiplies
+// it with its key chunk into partial frequency sums (both output polys) in its
+// own exchange buffers; after a CTA barrier warp-pairs 0 and 1 add the 2L
+// partials of output poly 0 / 1, run its inverse transform and update that
+// accumulator poly.  Same arithmetic, same rounding, same results as
+// pbs_blind_rotate_kernel; only the work split differs.
+template <int M, bool MODE_RAW, bool TRACK_MARGIN, int L2>
+__global__ void __launch_bounds__(L2 * (M / 8), 1)
+pbs_blind_rotate_wide_kernel(const PbsArgs args) {
+    constexpr int T = M / 8;
+    constexpr int PADM = PbsShape<M>::PADM;
+    constexpr int S = PbsRing<M>::S;
+    static_assert(L2 == S, "one ring stage per digit of a step");
+    constexpr uint32_t CHUNK = (uint32_t)pbs_chunk_bytes<M>();
+    constexpr int NT = L2 * T;
+    const DevParams& prm = args.prm;
+    constexpr int N = 2 * M;
+    const int n = prm.n;
+    constexpr int L = L2 / 2;
+    const uint32_t qmask = prm.qmask;
+    constexpr int log2_2N = (M == 256) ? 10 : (M == 512) ? 11 : 12;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+    uint64_t* empty = full + 4;
+    uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem_raw + 120);
+    double2* ring = reinterpret_cast<double2*>(smem_raw + 128);
+    const int warp = threadIdx.x / 32;
+    const int wp = threadIdx.x / T;  // warp-pair = digit index
+    const int t = threadIdx.x % T;
+    double2* bufs = reinterpret_cast<double2*>(smem_raw + 128 + S * CHUNK);
+    double2* buf0 = bufs + (size_t)wp * 2 * PADM;
+    double2* buf1 = buf0 + PADM;
+    int32_t* acc = reinterpret_cast<int32_t*>(bufs + (size_t)L2 * 2 * PADM);  // [2][N]
+    uint16_t* a2N = reinterpret_cast<uint16_t*>(acc + 2 * N);
+
+    const int64_t v = blockIdx.x;
+    const int64_t nchunks = (int64_t)n * L2;
+    const bool producer = threadIdx.x == 0;
+    if (producer) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], T);  // a chunk is read by one warp-pair
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc(tmem_base_slot, PBS_TMEM_COLS);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tbase = *tmem_base_slot;
+    const uint32_t lane_base = tbase + ((uint32_t)((warp % 4) * 32) << 16);
+    if (warp < 4) {  // per-lane twiddles + twist (t depends on the lane only)
+        TwiddlesInRegs<M> twr;
+        load_twiddles<M>(twr.tw, t, args.tables + M);
+#pragma unroll
+        for (int p = 1; p < Schedule<M>::P; ++p) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                double d[8];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const double2 w = twr.tw.w[p][4 * h + r < 7 ? 4 * h + r : 6];
+                    d[2 * r] = w.x;
+                    d[2 * r + 1] = w.y;
+                }
+                tmem_st16(lane_base + (p - 1) * 32 + 16 * h, d);
+            }
+        }
+        double2 twist[8];
+        load_twist<M>(twist, t, args.tables);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double d[8];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) { d[2 * r] = twist[4 * h + r].x; d[2 * r + 1] = twist[4 * h + r].y; }
+            tmem_st16(lane_base + PBS_TMEM_TWIST + 16 * h, d);
+        }
+        tmem_wait_st();
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+
+    if (producer) {
+        for (int s = 0; s < S && s < nchunks; ++s) {
+            mbar_arrive_expect_tx(&full[s], CHUNK);
+            bulk_g2s(ring + (size_t)s * 2 * M, args.bsk + (size_t)s * 2 * M, CHUNK, &full[s]);
+        }
+    }
+    // stage s always holds digit s of the current step; warp-pair s releases
+    // it after its MAC, and after the step's CTA barrier the producer loads
+    // the next step's chunks into all stages
+    auto refill = [&](int i) {
+        if (producer && (int64_t)(i + 1) * L2 < nchunks) {
+            for (int s = 0; s < S; ++s) {
+                mbar_wait(&empty[s], (uint32_t)(i & 1));
+                mbar_arrive_expect_tx(&full[s], CHUNK);
+                bulk_g2s(ring + (size_t)s * 2 * M, args.bsk + ((size_t)(i + 1) * L2 + s) * 2 * M, CHUNK, &full[s]);
+            }
+        }
+    };
+
+    const GroupSync gs{1 + wp, T};
+    const TwiddlesInTmem<M> tw{lane_base};
+    // ---------------- setup: modulus switch + accumulator init -------------
+    if constexpr (!MODE_RAW) {
+        const int u = (int)(v / args.count);
+        const int64_t row = v - (int64_t)u * args.count;
+        const uint32_t* a_in = args.in + row * prm.stride;
+        const uint32_t* a_in2 = args.in2 ? args.in2 + row * prm.stride : nullptr;
+        for (int i = threadIdx.x; i < n; i += NT) {
+            uint32_t a = a_in[i];
+            if (a_in2) a += a_in2[i];
+            a2N[i] = (uint16_t)rescale_q_to_2N(a, prm.log2q, log2_2N);
+        }
+        uint32_t b = a_in[n] + args.in_boff[u];
+        if (a_in2) b += a_in2[n];
+        const uint32_t b2N = (rescale_q_to_2N(b, prm.log2q, log2_2N) + prm.half_slot) & (2 * N - 1);
+        const int32_t* lut = args.lut[u];
+        for (int j = threadIdx.x; j < N; j += NT) {
+            acc[j] = 0;
+            const int src = (j + (int)b2N) & (2 * N - 1);
+            const int32_t val = lut[src & (N - 1)];
+            acc[N + j] = (int32_t)((uint32_t)(src >= N ? -val : val) & qmask);
+        }
+    } else {
+        const int32_t* a_src = args.acc_io + v * 2 * N;
+        for (int j = threadIdx.x; j < 2 * N; j += NT) acc[j] = (int32_t)((uint32_t)a_src[j] & qmask);
+        const int32_t* k_src = args.a2N_in + v * n;
+        for (int i = threadIdx.x; i < n; i += NT) a2N[i] = (uint16_t)(k_src[i] & (2 * N - 1));
+    }
+    __syncthreads();
+
+    const int bg = prm.bg_log;
+    const int32_t halfB1 = (1 << (bg - 1)) - 1;
+    const int32_t bmask = (1 << bg) - 1;
+    int32_t hsum = 0;
+#pragma unroll
+    for (int lvl = 0; lvl < L; ++lvl) hsum += halfB1 << (bg * lvl);
+    const uint32_t halfq = 1u << (prm.log2q - 1);
+    const int32_t yoff = hsum - (int32_t)halfq;
+    const int cc = wp / L, lvl = wp % L;
+    int ex = 0;
+    double err_max = 0.0;
+
+    for (int i = 0; i < n; ++i) {
+        const int k = a2N[i];
+        if (k == 0) {
+            mbar_wait(&full[wp], (uint32_t)(i & 1));
+            mbar_arrive(&empty[wp]);
+            __syncthreads();
+            refill(i);
+            continue;
+        }
+        // digit `lvl` of poly `cc` of (X^k - 1) * ACC
+        double2 vv[8];
+        {
+            const int32_t* a = acc + cc * N;
+            uint32_t twr[32];
+            tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
+            int32_t d1[8], d2[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int p = t + r * T;
+                const int s0 = (p - k) & (2 * N - 1), s1 = (p + M - k) & (2 * N - 1);
+                const uint32_t r0 = (s0 >= N) ? (uint32_t)(-a[s0 - N]) : (uint32_t)a[s0];
+                const uint32_t r1 = (s1 >= N) ? (uint32_t)(-a[s1 - N]) : (uint32_t)a[s1];
+                const int32_t y0 = (int32_t)((r0 - (uint32_t)a[p] + halfq) & qmask) + yoff;
+                const int32_t y1 = (int32_t)((r1 - (uint32_t)a[p + M] + halfq) & qmask) + yoff;
+                d1[r] = ((y0 >> (bg * lvl)) & bmask) - halfB1;
+                d2[r] = ((y1 >> (bg * lvl)) & bmask) - halfB1;
+            }
+            tmem_wait32(twr);
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                vv[r] = cmul(make_double2((double)d1[r], (double)d2[r]), words_c(twr, r));
+        }
+        fft_group<M, false>(vv, t, tw, buf0, buf1, ex, gs);
+        mbar_wait(&full[wp], (uint32_t)(i & 1));
+        const double2* kd = ring + (size_t)wp * 2 * M;
+        gs.sync();  // the transform's last exchange reads are done before the partials overwrite
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            double2 o0 = make_double2(0.0, 0.0), o1 = make_double2(0.0, 0.0);
+            cmac(o0, vv[r], kd[t + r * T]);
+            cmac(o1, vv[r], kd[M + t + r * T]);
+            buf0[t + r * T] = o0;  // partial sums of output poly 0
+            buf1[t + r * T] = o1;  // and 1
+        }
+        mbar_arrive(&empty[wp]);
+        __syncthreads();  // all partials written; every accumulator read of this step done
+        refill(i);
+        if (wp < 2) {  // warp-pair o inverse-transforms output poly o
+            const int o = wp;
+            double2 O[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                double2 sacc = bufs[(size_t)0 * 2 * PADM + o * PADM + t + r * T];
+#pragma unroll
+                for (int p = 1; p < L2; ++p) sacc = cadd(sacc, bufs[(size_t)p * 2 * PADM + o * PADM + t + r * T]);
+                O[r] = sacc;
+            }
+            named_bar(1 + L2, 2 * T);  // partial reads of warp-pairs 0/1 done before their buffers are reused
+            fft_group<M, true>(O, t, tw, buf0, buf1, ex, gs);
+            uint32_t twr[32];
+            tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
+            tmem_wait32(twr);
+            int32_t* a = acc + o * N;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int p = t + r * T;
+                const double2 z = cmulc(O[r], words_c(twr, r));
+                const long long r0 = round_product(z.x), r1 = round_product(z.y);
+                if constexpr (TRACK_MARGIN) {
+                    err_max = fmax(err_max, fabs(z.x - (double)r0));
+                    err_max = fmax(err_max, fabs(z.y - (double)r1));
+                }
+                a[p] = (int32_t)(((uint32_t)a[p] + (uint32_t)r0) & qmask);
+                a[p + M] = (int32_t)(((uint32_t)a[p + M] + (uint32_t)r1) & qmask);
+            }
+        }
+        __syncthreads();  // accumulator updated before the next step's reads
+    }
+    if constexpr (TRACK_MARGIN) {
+        if (args.margin) atomicMax(args.margin, (unsigned long long)__double_as_longlong(err_max));
+    }
+    if constexpr (MODE_RAW) {
+        int32_t* a_dst = args.acc_io + v * 2 * N;
+        for (int j = threadIdx.x; j < 2 * N; j += NT) a_dst[j] = acc[j];
+    } else {
+        uint32_t* out = args.ext_out + v * prm.ext_stride;
+        for (int j = threadIdx.x; j < N; j += NT) {
+            const uint32_t a = (j == 0) ? (uint32_t)acc[0] : ((uint32_t)(-acc[N - j]) & qmask);
+            out[j] = a;
+        }
+        if (threadIdx.x == 0) out[N] = (uint32_t)acc[N];
+    }
+    tmem_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tmem_fence_after();
+        tmem_dealloc(tbase, PBS_TMEM_COLS);
+    }
+}
+
+template <int M>
+__host__ __device__ constexpr size_t pbs_wide_smem_bytes(int L2, int N, int n) {
+    return 128 + (size_t)PbsRing<M>::S * pbs_chunk_bytes<M>() + (size_t)L2 * 2 * PbsShape<M>::PADM * sizeof(double2) +
+           2 * (size_t)N * sizeof(int32_t) + (((size_t)n * sizeof(uint16_t) + 15) & ~(size_t)15);
+}
+
 // Fourier transform of the bootstrapping key rows (BootstrapKey.__init__,
 // bootstrap.py:319-323): centred residues -> fold, twist, forward DFT, then
 // scaled by 1/M (exact) for the untwist-free epilogue above.

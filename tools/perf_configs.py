@@ -19,6 +19,18 @@ if "c3" in which or "c2" in which:
     g = neuron.g_fire(prm.p)
     lut = dev.lut(bootstrap.test_polynomial(g, prm))
 if "c3" in which:
+    peak_tf = dev.fp64_peak_tflops()
+    hbm_gbs, hbm_src = 7400.0, "B200_PROFILING.md fallback"
+    mp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        try:
+            d = json.load(open(mp))
+            for k, v in d.items():
+                if "hbm" in k.lower() and isinstance(v, (int, float)):
+                    hbm_gbs, hbm_src = float(v), f"MEASURED_PEAKS.json:{k}"
+                    break
+        except Exception:
+            pass
     sweep = {}
     for B in (1, 64, 1024, 16384, 131072):
         ms = W.pbs_messages(prm, B, seed=B)
@@ -33,8 +45,20 @@ if "c3" in which:
             dev.pbs_dev([lut], [0], [0], rows)
         e1.record(); torch.cuda.synchronize()
         ms_ = e0.elapsed_time(e1) / reps
-        sweep[B] = {"ms": ms_, "pbs_per_s": B / ms_ * 1e3}
+        # roofline of the whole PBS launch (blind rotation + key switch): FP64
+        # work 87.56 MFLOP/PBS vs the live DFMA peak; bytes = BSK + KSK read
+        # once per launch + input/output ciphertext rows
+        flops = B * 87556096
+        nbytes = (prm.n * 2 * prm.gadget.levels * 2 * (prm.N // 2) * 16
+                  + prm.N * prm.ks_levels * (prm.n + 1) * 4 + B * 2 * dev.stride * 4)
+        t_fp64 = flops / (peak_tf * 1e12)
+        t_hbm = nbytes / (hbm_gbs * 1e9)
+        sweep[B] = {"ms": ms_, "pbs_per_s": B / ms_ * 1e3,
+                    "fp64_tflops": flops / (ms_ * 1e-3) / 1e12, "hbm_gbs": nbytes / (ms_ * 1e-3) / 1e9,
+                    "bound": "fp64" if t_fp64 >= t_hbm else "hbm",
+                    "roofline_frac": max(t_fp64, t_hbm) / (ms_ * 1e-3)}
     out["config3_sweep"] = sweep
+    out["config3_peaks"] = {"fp64_tflops": peak_tf, "hbm_gbs": hbm_gbs, "hbm_source": hbm_src}
 if "c2" in which:
     lif = W.lif_for(api, prm)
     net = W.config2_network(api, lif)
