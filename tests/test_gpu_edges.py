@@ -121,3 +121,18 @@ def test_fdsn_containers_to_device(toy, toy_keys, tmp_path):
     assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
     with pytest.raises(errors.ParameterError):
         serial.load_bootstrap_key_device(tmp_path / "ct.bin", toy)
+
+
+@pytest.mark.parametrize("count", [148, 149, 296, 297])
+def test_launch_regime_boundaries(desk, desk_keys, count):
+    """Batches either side of the latency-kernel / 1-rotation-CTA / 4-rotation-CTA
+    switch points give oracle-identical outputs (first and last 6 checked)."""
+    sk, _, bsk = desk_keys
+    rng = np.random.default_rng(count)
+    A, b = lwe.encrypt_batch(rng.integers(-511, 513, count), sk, desk, rng)
+    g = neuron.g_fire(desk.p)
+    oA, ob = bootstrap.bootstrap_batch(g, A, b, bsk)
+    key = oracle_key(desk, bsk)
+    for sl in (slice(0, 6), slice(count - 6, count)):
+        wA, wb = O.bootstrap_batch(g.table, A[sl], b[sl], key)
+        assert np.array_equal(oA[sl], wA) and np.array_equal(ob[sl], wb)
