@@ -8,7 +8,7 @@ reference.  Run:
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
         python tests/golden/make_golden.py [section ...]
 
-Sections: keys toy toy64 desk c4 layer config0 config1 config2 fdsn plain
+Sections: keys toy toy64 desk c4 layer config0 config1 config2 fdsn plain paper
 """
 
 from __future__ import annotations
@@ -256,6 +256,39 @@ def sec_plain():
     save("plain", **out)
 
 
+def sec_paper():
+    """The paper's own network: the reference fixture model model_if_t2.json
+    (conv 10x8x8/2 -> IF -> avgpool 2 -> fc 360->160 -> IF -> fc 160->10 -> IF,
+    T=2) discretized at theta=40 on DESK with p=2048 (the parameter set of the
+    reference's desk_eval.json, digest d71006c1...), keys seed 0, two synthetic
+    images.  Saves the model weights (with the fixture's sha256) and the
+    reference's encrypted-inference outputs."""
+    path = "/root/reference/pkg/tests/fixtures/model_if_t2.json"
+    with open(path, "rb") as f:
+        model_sha = hashlib.sha256(f.read()).hexdigest()
+    model = fdsnn.network.CsnnModel.load(path)
+    net = fdsnn.network.discretize(model, 40)
+    prm = fdsnn.params.preset("DESK").with_p(2048)
+    sk, zk, bsk = W.keys(fdsnn, prm, 0)
+    imgs = W.synth_images(2)
+    encs = W.encrypt_images(fdsnn, prm, sk, imgs)
+    out = {}
+    for k, enc in enumerate(encs):
+        t0 = time.time()
+        scores, stats = fdsnn.network.infer(enc, net, bsk, workers=8)
+        print(f"paper image {k}: {stats.bootstrap_count} PBS in {time.time() - t0:.1f}s")
+        out[f"score_digest{k}"] = np.frombuffer(bytes.fromhex(sha(scores.A, scores.b)), np.uint8)
+        out[f"scores{k}"] = fdsnn.lwe.decrypt_batch(scores.A, scores.b, sk, prm)
+        out[f"boots{k}"] = np.array([stats.bootstrap_count])
+        plain, _ = fdsnn.oracle.plain_infer(net, imgs[k].astype(np.float64) / 255.0, p=prm.p)
+        out[f"plain{k}"] = plain
+    save("paper", model_sha256=np.frombuffer(bytes.fromhex(model_sha), np.uint8),
+         params_digest=np.frombuffer(bytes.fromhex(prm.digest()), np.uint8), **out)
+    w = {f"w{i}": np.asarray(x, np.float64) for i, x in enumerate(model.weights)}
+    save("paper_model", T=np.array([model.T]), L=np.array([model.L]), v_th=np.array([model.v_th]),
+         model_sha256=np.frombuffer(bytes.fromhex(model_sha), np.uint8), **w)
+
+
 def sec_fdsn():
     """sha256 of FDSN containers written by the reference (TOY keys seed 1)."""
     import tempfile
@@ -285,7 +318,7 @@ SECTIONS = {
     "desk": lambda: sec_lif(W.desk1024(fdsnn), "desk_lif", 32),
     "c4": lambda: sec_lif(W.c4_params(fdsnn), "c4_lif", 4),
     "layer": sec_layer, "config0": sec_config0, "config1": sec_config1, "config2": sec_config2,
-    "plain": sec_plain,
+    "plain": sec_plain, "paper": sec_paper,
 }
 
 if __name__ == "__main__":

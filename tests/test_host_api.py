@@ -191,3 +191,33 @@ def test_fdsn_containers_byte_identical_to_reference(toy, toy_keys, tmp_path):
         serial.load_ciphertexts(tmp_path / "ct.bin", params.preset("DESK"))
     with pytest.raises(errors.SerializationError):
         serial.load_secret_key(tmp_path / "ct.bin", toy)
+
+
+def _paper_model():
+    from paper_2309_09025_b200 import network as N
+    m = np.load(os.path.join(GOLDEN, "paper_model.npz"))
+    arch = ({"type": "conv2d", "out_channels": 10, "kernel": [8, 8], "stride": [2, 2], "padding": [1, 1]},
+            {"type": "spiking"}, {"type": "avgpool", "window": [2, 2]},
+            {"type": "linear", "out_features": 160}, {"type": "spiking"},
+            {"type": "linear", "out_features": 10}, {"type": "spiking"})
+    return N.CsnnModel(arch=arch, weights=(m["w0"], m["w1"], m["w2"]), input_shape=(1, 28, 28),
+                       T=int(m["T"][0]), L=int(m["L"][0]), tau=None, v_th=float(m["v_th"][0]))
+
+
+def test_paper_model_lowering_known_answers():
+    """The paper's network (reference fixture model_if_t2.json, weights in
+    tests/golden/paper_model.npz) discretized at theta=40: 3220 PBS per step
+    (reference test_oracle.py:175) and the reference's plain_infer scores."""
+    from paper_2309_09025_b200 import network as N
+    net = N.discretize(_paper_model(), 40)
+    assert net.bootstrap_count(1) == 3220 and net.bootstrap_count(2) == 6440
+    g = np.load(os.path.join(GOLDEN, "paper.npz"))
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(GOLDEN), os.pardir, "tools"))
+    import workloads as W
+    from conftest import O
+    layers = W.layers_for_oracle(net)
+    for k, img in enumerate(W.synth_images(2)):
+        x = (img.astype(np.float64) / 255.0 >= 0.5).astype(np.int64).ravel()
+        sc, _, over = O.plain_infer(x, layers, net.T, 2048)
+        assert over == 0 and np.array_equal(sc, g[f"plain{k}"])
