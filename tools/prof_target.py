@@ -7,15 +7,15 @@ from paper_2309_09025_b200 import bootstrap, lwe, neuron, params, rgsw
 from paper_2309_09025_b200.bootstrap import test_polynomial
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1184
-prm = params.preset("DESK").with_p(1024)
+prm = params.c4() if os.environ.get("PROBE_PARAMS") == "c4" else params.preset("DESK").with_p(1024)
 rng = np.random.default_rng(0)
 sk = lwe.lwe_keygen(prm, rng); zk = rgsw.rlwe_keygen(prm, rng)
 bsk = bootstrap.gen_bootstrap_key(sk, zk, prm, rng)
 dev = bsk.device
-lif = neuron.LifParams(tau=2, theta=64)
+lif = neuron.LifParams(tau=2, theta=256 if prm.p == 4096 else 64)
 lf = dev.lut(test_polynomial(neuron.g_fire(prm.p), prm))
 lr = dev.lut(test_polynomial(neuron.g_reset(lif, prm.p), prm))
-A, b = lwe.encrypt_batch(rng.integers(-511, 513, B), sk, prm, rng)
+A, b = lwe.encrypt_batch(rng.integers(-prm.p // 2 + 1, prm.p // 2 + 1, B), sk, prm, rng)
 rows = dev.rows_from_host(A, b)
 zero = dev.zero_rows(B)
 for _ in range(2):
