@@ -11,13 +11,26 @@ import paper_2309_09025_b200 as api
 from paper_2309_09025_b200 import bootstrap, network, neuron
 
 out = {}
-which = sys.argv[1:] or ["c3", "c2", "c4"]
-if "c3" in which or "c2" in which:
+which = sys.argv[1:] or ["c0", "c3", "c2", "c4"]
+if "c0" in which or "c3" in which or "c2" in which:
     prm = W.desk1024(api)
     sk, zk, bsk = W.keys(api, prm)
     dev = bsk.device
     g = neuron.g_fire(prm.p)
     lut = dev.lut(bootstrap.test_polynomial(g, prm))
+if "c0" in which:
+    # config 0: 1024 LIF bootstraps (fire + reset = 2048 PBS with key switch), one fused launch
+    lif0 = W.lif_for(api, prm)
+    A0, b0 = W.encrypt(api, prm, sk, W.pbs_messages(prm, 1024))
+    zeros = np.zeros_like(A0), np.zeros_like(b0)
+    neuron.fhe_lif_step_batch(zeros[0], zeros[1], A0, b0, lif0, bsk)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    reps = 5
+    for _ in range(reps):
+        neuron.fhe_lif_step_batch(zeros[0], zeros[1], A0, b0, lif0, bsk)
+    dt = (time.perf_counter() - t0) / reps
+    out["config0"] = {"pbs": 2048, "ms_host_to_host": dt * 1e3, "pbs_per_s": 2048 / dt}
 if "c3" in which:
     peak_tf = dev.fp64_peak_tflops()
     hbm_gbs, hbm_src = 7400.0, "B200_PROFILING.md fallback"
