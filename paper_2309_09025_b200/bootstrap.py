@@ -22,7 +22,7 @@ import numpy as np
 
 from .errors import DomainError, ParameterError
 from .lwe import LweCiphertext, LweSecretKey, sample_noise
-from .params import FheParams, GadgetParams
+from .params import FheParams
 from .rgsw import RgswCiphertext, RlweCiphertext, RlweSecretKey, rgsw_encrypt_bit
 from .ring import monomial_rotate_raw
 

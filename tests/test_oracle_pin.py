@@ -6,7 +6,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, O, make_keys, oracle_key
+from conftest import GOLDEN, O, oracle_key
 from paper_2309_09025_b200 import lwe, neuron, params
 
 
