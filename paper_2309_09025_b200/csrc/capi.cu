@@ -875,8 +875,14 @@ int fdsnn_operator_apply(fdsnn_ctx* ctx, int32_t op_id, const uint32_t* d_in, in
     const DevParams& d = ctx->dp;
     TimerScope ts(ctx, 2, s);
     if (op.dense) {
-        dim3 grid((op.out_cells + LIN_ROWS - 1) / LIN_ROWS, (d.stride + LIN_COLS - 1) / LIN_COLS, (unsigned)batch);
-        linear_dense_kernel<<<grid, 256, 0, s>>>(op.w, op.out_cells, op.in_cells, d_in, d_out, d.stride, d.qmask);
+        const int64_t big = (int64_t)((op.out_cells + LIN_ROWS - 1) / LIN_ROWS) * ((d.stride + LIN_COLS - 1) / LIN_COLS) * batch;
+        if (big < 2 * 148) {  // small operator: half-height tiles, twice the CTAs
+            dim3 grid((op.out_cells + 31) / 32, (d.stride + LIN_COLS - 1) / LIN_COLS, (unsigned)batch);
+            linear_dense_kernel<4><<<grid, 256, 0, s>>>(op.w, op.out_cells, op.in_cells, d_in, d_out, d.stride, d.qmask);
+        } else {
+            dim3 grid((op.out_cells + LIN_ROWS - 1) / LIN_ROWS, (d.stride + LIN_COLS - 1) / LIN_COLS, (unsigned)batch);
+            linear_dense_kernel<8><<<grid, 256, 0, s>>>(op.w, op.out_cells, op.in_cells, d_in, d_out, d.stride, d.qmask);
+        }
     } else {
         dim3 grid(op.out_cells, (unsigned)batch);
         linear_csr_kernel<<<grid, 160, 0, s>>>(op.row_ptr, op.col_idx, op.val, op.out_cells, op.in_cells, d_in, d_out, d.stride, d.qmask);

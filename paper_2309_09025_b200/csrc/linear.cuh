@@ -18,27 +18,31 @@ constexpr int LIN_ROWS = 64;
 constexpr int LIN_COLS = 128;
 constexpr int LIN_K = 16;
 
-// Dense: Wm (out x in) int32 row-major; X batch-stacked rows (batch*in x stride)
-template <bool DUMMY = false>
+// Dense: Wm (out x in) int32 row-major; X batch-stacked rows (batch*in x stride).
+// A CTA computes RPT*8 output rows x LIN_COLS columns (8 warps, each thread
+// RPT rows x 4 columns); RPT = 8 for large operators, 4 when the grid would
+// otherwise fill less than two waves of SMs.
+template <int RPT = 8>
 __global__ void __launch_bounds__(256)
 linear_dense_kernel(const int32_t* __restrict__ Wm, int out_cells, int in_cells,
                     const uint32_t* __restrict__ X, uint32_t* __restrict__ Y,
                     int stride, uint32_t qmask) {
-    __shared__ __align__(16) int32_t ws[LIN_K][LIN_ROWS];
+    constexpr int TR = 8 * RPT;
+    __shared__ __align__(16) int32_t ws[LIN_K][TR];
     __shared__ __align__(16) uint32_t xs[LIN_K][LIN_COLS];
     const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
-    const int r0 = blockIdx.x * LIN_ROWS;
+    const int r0 = blockIdx.x * TR;
     const int c0 = blockIdx.y * LIN_COLS;
     const int bidx = blockIdx.z;
     const uint32_t* Xb = X + (size_t)bidx * in_cells * stride;
     uint32_t* Yb = Y + (size_t)bidx * out_cells * stride;
-    uint32_t acc[8][4];
+    uint32_t acc[RPT][4];
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+    for (int a = 0; a < RPT; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0u;
     for (int k0 = 0; k0 < in_cells; k0 += LIN_K) {
-        for (int e = threadIdx.x; e < LIN_K * LIN_ROWS; e += blockDim.x) {
+        for (int e = threadIdx.x; e < LIN_K * TR; e += blockDim.x) {
             const int rr = e / LIN_K, kk = e % LIN_K;
             const int r = r0 + rr, k = k0 + kk;
             ws[kk][rr] = (r < out_cells && k < in_cells) ? Wm[(size_t)r * in_cells + k] : 0;
@@ -54,21 +58,24 @@ linear_dense_kernel(const int32_t* __restrict__ Wm, int out_cells, int in_cells,
         __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < LIN_K; ++kk) {
-            const int4 w0 = *reinterpret_cast<const int4*>(&ws[kk][ty * 8]);
-            const int4 w1 = *reinterpret_cast<const int4*>(&ws[kk][ty * 8 + 4]);
+            int32_t wd[RPT];
+#pragma unroll
+            for (int a = 0; a < RPT; a += 4) {
+                const int4 w4 = *reinterpret_cast<const int4*>(&ws[kk][ty * RPT + a]);
+                wd[a] = w4.x; wd[a + 1] = w4.y; wd[a + 2] = w4.z; wd[a + 3] = w4.w;
+            }
             const uint4 xv = *reinterpret_cast<const uint4*>(&xs[kk][tx * 4]);
-            const int32_t wd[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
             const uint32_t xd[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
-            for (int a = 0; a < 8; ++a)
+            for (int a = 0; a < RPT; ++a)
 #pragma unroll
                 for (int b = 0; b < 4; ++b) acc[a][b] += (uint32_t)wd[a] * xd[b];
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-        const int r = r0 + ty * 8 + a;
+    for (int a = 0; a < RPT; ++a) {
+        const int r = r0 + ty * RPT + a;
         if (r >= out_cells) continue;
         const int c = c0 + tx * 4;
         if (c < stride) {
