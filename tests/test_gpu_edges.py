@@ -136,3 +136,19 @@ def test_launch_regime_boundaries(desk, desk_keys, count):
     for sl in (slice(0, 6), slice(count - 6, count)):
         wA, wb = O.bootstrap_batch(g.table, A[sl], b[sl], key)
         assert np.array_equal(oA[sl], wA) and np.array_equal(ob[sl], wb)
+
+
+def test_large_preset_bit_exact():
+    """The reference's LARGE preset (n=1024, q=2^27, N=2048, Bg=2^10 l=3, KS
+    2^5x6): a different modulus, gadget and key-switch shape from every other
+    test (4-limb tensor-core key switch with K=12288, n=1024 columns)."""
+    from conftest import make_keys
+    from paper_2309_09025_b200 import params
+    prm = params.preset("LARGE")
+    sk, _, bsk = make_keys(prm, 3)
+    rng = np.random.default_rng(3)
+    A, b = lwe.encrypt_batch(rng.integers(-prm.p // 2 + 1, prm.p // 2 + 1, 3), sk, prm, rng)
+    g = neuron.g_fire(prm.p)
+    oA, ob = bootstrap.bootstrap_batch(g, A, b, bsk)
+    wA, wb = O.bootstrap_batch(g.table, A, b, oracle_key(prm, bsk))
+    assert np.array_equal(oA, wA) and np.array_equal(ob, wb)
