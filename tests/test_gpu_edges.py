@@ -152,3 +152,23 @@ def test_large_preset_bit_exact():
     oA, ob = bootstrap.bootstrap_batch(g, A, b, bsk)
     wA, wb = O.bootstrap_batch(g.table, A, b, oracle_key(prm, bsk))
     assert np.array_equal(oA, wA) and np.array_equal(ob, wb)
+
+
+def test_n1024_three_level_gadget_paths():
+    """N=1024 with a 3-level gadget (Bg=2^9): the single-level transform
+    kernels at M=512 (1-rotation CTAs below 297 rotations, 4-rotation CTAs
+    above), which the DESK gadget (l=2) never selects."""
+    from dataclasses import replace
+    from conftest import make_keys
+    from paper_2309_09025_b200 import params
+    prm = replace(params.preset("DESK").with_p(1024), gadget=params.GadgetParams(1 << 9, 3), preset_name="custom")
+    sk, _, bsk = make_keys(prm, 4)
+    key = oracle_key(prm, bsk)
+    g = neuron.g_fire(prm.p)
+    rng = np.random.default_rng(4)
+    for count in (5, 300):
+        A, b = lwe.encrypt_batch(rng.integers(-511, 513, count), sk, prm, rng)
+        oA, ob = bootstrap.bootstrap_batch(g, A, b, bsk)
+        for sl in (slice(0, 3), slice(count - 3, count)):
+            wA, wb = O.bootstrap_batch(g.table, A[sl], b[sl], key)
+            assert np.array_equal(oA[sl], wA) and np.array_equal(ob[sl], wb), count
