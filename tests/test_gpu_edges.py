@@ -172,3 +172,18 @@ def test_n1024_three_level_gadget_paths():
         for sl in (slice(0, 3), slice(count - 3, count)):
             wA, wb = O.bootstrap_batch(g.table, A[sl], b[sl], key)
             assert np.array_equal(oA[sl], wA) and np.array_equal(ob[sl], wb), count
+
+
+@pytest.mark.parametrize("count", [5, 400])
+def test_desk_blind_rotate_raw_mode(desk, desk_keys, count):
+    """blind_rotate_batch at DESK through the latency kernel (5) and the paired
+    kernel (400), raw accumulators in and out, vs the oracle (3 checked)."""
+    sk, _, bsk = desk_keys
+    rng = np.random.default_rng(40 + count)
+    acc = rng.integers(0, desk.q, (count, 2, desk.N))
+    a2N = rng.integers(0, 2 * desk.N, (count, desk.n))
+    got = bootstrap.blind_rotate_batch(acc, a2N, bsk)
+    key = oracle_key(desk, bsk)
+    for j in (0, count // 2, count - 1):
+        want = O.blind_rotate(acc[j:j + 1], a2N[j:j + 1], key)
+        assert np.array_equal(got[j:j + 1], want), j
