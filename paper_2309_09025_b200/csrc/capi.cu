@@ -102,6 +102,7 @@ struct fdsnn_ctx {
     struct StreamScratch { Buf ext, ks_dig; };
     std::map<cudaStream_t, StreamScratch> scratch;
     int64_t wide_max = 148;  // largest batch routed to the latency kernel (FDSNN_WIDE_MAX)
+    int64_t sm_count = 148;
     bool keys_loaded = false;
     std::vector<int32_t*> luts;
     std::vector<Operator> ops;
@@ -145,6 +146,7 @@ cudaStream_t pick(fdsnn_ctx* ctx, void* stream) {
     return stream ? reinterpret_cast<cudaStream_t>(stream) : cudaStreamLegacy;
 }
 
+// V = rotations covered by this launch, starting at a.v_base
 template <int M, int G, bool RAW, bool MARGIN, bool PAIR>
 int launch_br_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_t s) {
     const size_t smem = pbs_smem_bytes<M>(G, 2 * M, ctx->dp.n);
@@ -185,14 +187,28 @@ int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_
             // (G=1 CTAs are small enough for 2 per SM: <= 296 rotations fit in one wave)
             // gadget levels L == 2 (DESK): the paired-level transform variant
             if (ctx->dp.L == 2) {
-                if (V <= ctx->wide_max) {  // latency regime: one CTA per rotation, digits in parallel
-                    if (raw) return ctx->track_margin ? launch_br_wide_t<true, true>(ctx, a, V, s)
-                                                      : launch_br_wide_t<true, false>(ctx, a, V, s);
-                    return ctx->track_margin ? launch_br_wide_t<false, true>(ctx, a, V, s)
-                                             : launch_br_wide_t<false, false>(ctx, a, V, s);
+                // Rounds of 4 rotations per SM, then the remainder at the
+                // density that finishes it fastest: 1/SM on the latency
+                // kernel, 2 or 3 per SM, or folded into the 4/SM launch.
+                const int64_t sms = ctx->sm_count, round4 = 4 * sms;
+                int64_t rem = V % round4, full = V - rem;
+                if (rem > 3 * sms) { full = V; rem = 0; }
+                ts.kernels = (full > 0) + (rem > 0);
+                if (full > 0) {
+                    int rc = launch_br_m<512, 4, true>(ctx, a, full, raw, s);
+                    if (rc) return rc;
                 }
-                if (V > 2 * 148) return launch_br_m<512, 4, true>(ctx, a, V, raw, s);
-                return launch_br_m<512, 1, true>(ctx, a, V, raw, s);
+                if (rem == 0) return FDSNN_OK;
+                PbsArgs t = a;
+                t.v_base = a.v_base + full;
+                if (rem <= ctx->wide_max) {  // latency regime: one CTA per rotation, digits in parallel
+                    if (raw) return ctx->track_margin ? launch_br_wide_t<true, true>(ctx, t, rem, s)
+                                                      : launch_br_wide_t<true, false>(ctx, t, rem, s);
+                    return ctx->track_margin ? launch_br_wide_t<false, true>(ctx, t, rem, s)
+                                             : launch_br_wide_t<false, false>(ctx, t, rem, s);
+                }
+                if (rem <= 2 * sms) return launch_br_m<512, 2, true>(ctx, t, rem, raw, s);
+                return launch_br_m<512, 3, true>(ctx, t, rem, raw, s);
             }
             if (V > 2 * 148) return launch_br_m<512, 4>(ctx, a, V, raw, s);
             return launch_br_m<512, 1>(ctx, a, V, raw, s);
@@ -407,6 +423,7 @@ int fdsnn_ctx_create(const fdsnn_params* prm, int32_t device, fdsnn_ctx** out) {
     ctx->prm = p;
     ctx->device = device;
     ctx->wide_max = dprop.multiProcessorCount;
+    ctx->sm_count = dprop.multiProcessorCount;
     if (const char* e = getenv("FDSNN_WIDE_MAX")) ctx->wide_max = atoll(e);
     DevParams& d = ctx->dp;
     d.n = p.n;

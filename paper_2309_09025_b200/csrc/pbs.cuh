@@ -41,6 +41,7 @@ struct PbsArgs {
     const uint32_t* in2;   // optional second operand added to `in` (LIF charge)
     int64_t count;         // rows per LUT
     int nlut;              // virtual ciphertexts = nlut * count
+    int64_t v_base;        // first virtual ciphertext of this launch (a launch may cover a sub-range)
     const int32_t* lut[4]; // device test polynomials (N residues)
     uint32_t in_boff[4];   // added to b before the modulus switch (mod q)
     // input mode B: raw accumulators + rotation indices (blind_rotate_batch)
@@ -130,7 +131,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     uint16_t* a2N = reinterpret_cast<uint16_t*>(acc + 2 * N);
 
     const int64_t V = (int64_t)args.nlut * args.count;
-    const int64_t v0 = (int64_t)blockIdx.x * G;
+    const int64_t v0 = args.v_base + (int64_t)blockIdx.x * G;
     const int nact = (int)((V - v0) < G ? (V - v0) : G);  // active groups in this CTA
     const bool active = g < nact;
     const int64_t nchunks = (int64_t)n * 2 * L;
@@ -501,7 +502,7 @@ pbs_blind_rotate_wide_kernel(const PbsArgs args) {
     int32_t* acc = reinterpret_cast<int32_t*>(bufs + (size_t)L2 * 2 * PADM);  // [2][N]
     uint16_t* a2N = reinterpret_cast<uint16_t*>(acc + 2 * N);
 
-    const int64_t v = blockIdx.x;
+    const int64_t v = args.v_base + blockIdx.x;
     const int64_t nchunks = (int64_t)n * L2;
     const bool producer = threadIdx.x == 0;
     if (producer) {

@@ -123,10 +123,11 @@ def test_fdsn_containers_to_device(toy, toy_keys, tmp_path):
         serial.load_bootstrap_key_device(tmp_path / "ct.bin", toy)
 
 
-@pytest.mark.parametrize("count", [148, 149, 296, 297])
+@pytest.mark.parametrize("count", [148, 149, 296, 297, 445, 600, 740, 1040])
 def test_launch_regime_boundaries(desk, desk_keys, count):
-    """Batches either side of the latency-kernel / 1-rotation-CTA / 4-rotation-CTA
-    switch points give oracle-identical outputs (first and last 6 checked)."""
+    """Batches either side of the launch-split points (full rounds of 4
+    rotations per SM, remainder on the latency kernel or at 2-3 per SM) give
+    oracle-identical outputs (first and last 6 checked)."""
     sk, _, bsk = desk_keys
     rng = np.random.default_rng(count)
     A, b = lwe.encrypt_batch(rng.integers(-511, 513, count), sk, desk, rng)
