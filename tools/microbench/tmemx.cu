@@ -69,7 +69,7 @@ __global__ void k_layout(uint32_t* out) {
 }
 
 // MODE 0: shared-memory exchange, 1: one TMEM hop, 2: two TMEM hops
-template <int MODE>
+template <int MODE0>
 __global__ void __launch_bounds__(256, 1) k_ex(double* out, int iters) {
     __shared__ uint32_t tb;
     __shared__ double2 buf[8][288];  // per warp 256 complex + pad
@@ -78,6 +78,8 @@ __global__ void __launch_bounds__(256, 1) k_ex(double* out, int iters) {
     const uint32_t ta = t + ((uint32_t)((w % 4) * 32) << 16) + (uint32_t)((w / 4) * 64);
     double2 x[8];
     for (int r = 0; r < 8; ++r) x[r] = make_double2(i + r, i - r);
+    // MODE0 3: half the warps exchange through smem, the other half hop through TMEM
+    const int MODE = MODE0 == 3 ? (w < 4 ? 0 : 1) : MODE0;
     for (int it = 0; it < iters; ++it) {
         if (MODE == 0) {
             double2* b = buf[w];
@@ -89,7 +91,7 @@ __global__ void __launch_bounds__(256, 1) k_ex(double* out, int iters) {
             __syncwarp();
         } else {
 #pragma unroll
-            for (int h = 0; h < MODE; ++h) {
+            for (int h = 0; h < (MODE0 == 3 ? 1 : MODE0); ++h) {
                 uint32_t v[32];
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
@@ -153,13 +155,14 @@ int main() {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     const int iters = 4000;
-    const char* names[3] = {"smem", "tmem 1 hop", "tmem 2 hops"};
-    for (int mode = 0; mode < 3; ++mode)
+    const char* names[4] = {"smem", "tmem 1 hop", "tmem 2 hops", "4 warps smem + 4 warps tmem"};
+    for (int mode = 0; mode < 4; ++mode)
         for (int threads : {32, 256}) {
             auto run = [&](int it) {
                 if (mode == 0) k_ex<0><<<148, threads>>>(d, it);
                 if (mode == 1) k_ex<1><<<148, threads>>>(d, it);
                 if (mode == 2) k_ex<2><<<148, threads>>>(d, it);
+                if (mode == 3) k_ex<3><<<148, threads>>>(d, it);
             };
             run(10);
             cudaEventRecord(a);
