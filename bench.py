@@ -289,10 +289,12 @@ def run_b200(args, world, rank, local):
     br_launch_ms = br_ms / max(br_n, 1)
     pbs_per_launch = BATCH * NEURONS * 2
     achieved = FLOPS_PER_PBS_DESK * pbs_per_launch / (br_launch_ms * 1e-3) / 1e12
-    traffic = None
+    traffic, pipe_active = None, None
     tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("bytes_per_launch")
+        tj = json.load(open(tpath))
+        traffic = tj.get("bytes_per_launch")
+        pipe_active = tj.get("fp64_pipe_active")
     if rank != 0:
         return
     line = {
@@ -310,6 +312,7 @@ def run_b200(args, world, rank, local):
         "gpu_launches": int(br_n + ks_n + lin_n),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "fp64_pipe_active": pipe_active,
                      "kernel": "pbs_blind_rotate_kernel<512,4>",
                      "flops_per_pbs": FLOPS_PER_PBS_DESK, "pbs_per_launch": pbs_per_launch,
                      "peak_source": "DFMA loop measured live in this run (fdsnn_probe_fp64_peak); "
