@@ -175,15 +175,23 @@ def cpu_oracle_pbs_per_s(neurons_per_core: int = 48):
     cores = len(os.sched_getaffinity(0))
     _pin_single_thread()  # inherited by the spawned workers: one thread per process
     with get_context("spawn").Pool(cores) as pool:
-        t0 = time.perf_counter()
-        res = pool.map(_oracle_worker, [(neurons_per_core, 100 + c) for c in range(cores)])
-        wall = time.perf_counter() - t0
+        # best of two passes: host-side noise (other tenants, frequency ramps)
+        # otherwise swings the slowest-process time by +-30 % between runs
+        best = None
+        for _ in range(2):
+            t0 = time.perf_counter()
+            res = pool.map(_oracle_worker, [(neurons_per_core, 100 + c) for c in range(cores)])
+            wall = time.perf_counter() - t0
+            compute = max(r[1] for r in res)
+            if best is None or compute < best[1]:
+                best = (res, compute, wall)
+        res, compute, wall = best
     pbs = sum(r[0] for r in res)
-    compute = max(r[1] for r in res)
     return {"value": pbs / compute, "unit": "PBS/s", "cores": cores, "kind": "port",
             "sample": f"{pbs} PBS: fused LIF step (fire+reset, with key switch) on {neurons_per_core} "
                       f"DESK p=1024 neurons per core, {cores} processes, numba+numpy oracle port of "
-                      f"bootstrap.py:517-534 / neuron.py:700-712; timed region excludes keygen",
+                      f"bootstrap.py:517-534 / neuron.py:700-712; timed region excludes keygen; "
+                      f"slowest process of the better of two passes",
             "wall_s": round(wall, 2)}
 
 
