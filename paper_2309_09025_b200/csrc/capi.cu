@@ -454,8 +454,10 @@ int fdsnn_ctx_create(const fdsnn_params* prm, int32_t device, fdsnn_ctx** out) {
         tab[k] = make_double2((double)cosl(tw), (double)sinl(tw));
     }
     {
-        const int* radix = M == 256 ? Schedule<256>::R : M == 512 ? Schedule<512>::R : Schedule<1024>::R;
-        const int P = M == 1024 ? 4 : 3;
+        // M = 1024 runs as two 512-point transforms (fft.cuh parity split):
+        // the M = 512 pass twiddles, then the radix-2 join factors below
+        const int* radix = M == 256 ? Schedule<256>::R : Schedule<512>::R;
+        const int P = 3;
         int ns = radix[0];
         for (int pass = 1; pass < P; ++pass) {
             const int R = radix[pass];
@@ -466,6 +468,11 @@ int fdsnn_ctx_create(const fdsnn_params* prm, int32_t device, fdsnn_ctx** out) {
                 }
             ns *= R;
         }
+        if (M == 1024)
+            for (int k = 0; k < 512; ++k) {
+                long double ang = 2.0L * PI * k / 1024.0L;
+                tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+            }
     }
     if (cudaMalloc(&ctx->tables, tab.size() * sizeof(double2)) != cudaSuccess ||
         cudaMemcpy(ctx->tables, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -516,7 +523,8 @@ int fdsnn_bsk_load(fdsnn_ctx* ctx, const int64_t* rows, const int64_t* ksk_A, co
         const int M = d.M;
         const int T = M / 8;
         const int G = 128 / T > 0 ? 128 / T : 1;
-        const size_t smem = (size_t)G * 2 * (M + M / 8) * sizeof(double2);
+        const size_t padm = M == 1024 ? PbsShape<1024>::PADM : M == 512 ? PbsShape<512>::PADM : PbsShape<256>::PADM;
+        const size_t smem = (size_t)G * 2 * padm * sizeof(double2);
         const unsigned blocks = (unsigned)((npoly + G - 1) / G);
         switch (M) {
             case 256:

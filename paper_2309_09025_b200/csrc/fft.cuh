@@ -234,9 +234,9 @@ struct NoHook {
 // pass's arithmetic
 // (used to start the key fetch of the following MAC).
 template <int M, bool INV, class TW, class HOOK = NoHook>
-FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
-                         double2* __restrict__ buf0, double2* __restrict__ buf1,
-                         int& ex, const GroupSync& gs, const HOOK& pre_last = HOOK()) {
+FDSNN_DEV void fft_stockham(double2 (&v)[8], int t, const TW& tw,
+                            double2* __restrict__ buf0, double2* __restrict__ buf1,
+                            int& ex, const GroupSync& gs, const HOOK& pre_last = HOOK()) {
     constexpr int P = Schedule<M>::P;
     {
         double2 w[8];
@@ -267,9 +267,9 @@ FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
 // sides (write-after-read on the buffers), so it is safe whatever the buffers
 // were last used for.
 template <int M, bool INV, class TW, class HOOK = NoHook>
-FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& tw,
-                          double2* __restrict__ buf0, double2* __restrict__ buf1,
-                          const GroupSync& gs, const HOOK& pre_last = HOOK()) {
+FDSNN_DEV void fft_stockham2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& tw,
+                             double2* __restrict__ buf0, double2* __restrict__ buf1,
+                             const GroupSync& gs, const HOOK& pre_last = HOOK()) {
     constexpr int P = Schedule<M>::P;
     {
         double2 w[8];
@@ -296,6 +296,128 @@ FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& t
     FDSNN_FFT2_STEP(2)
     FDSNN_FFT2_STEP(3)
 #undef FDSNN_FFT2_STEP
+}
+
+// ---------------------------------------------------------------------------
+// M = 1024 as a parity split (C4, N = 2048): thread t = 2t' + p holds the
+// points {t + 128 r} = {2(t' + 64 r) + p}, i.e. the 512-point subsequence of
+// parity p at the positions the 64-thread M = 512 transform expects.  The two
+// 512-point transforms (2 shared-memory exchanges each, run side by side by
+// the even and odd lanes, each parity in its own half of the exchange
+// buffers) are joined by one radix-2 step between lanes 2t' and 2t'+1 through
+// warp shuffles:  X[k] = E[k] + w^k O[k],  X[k + 512] = E[k] - w^k O[k]
+// (w = e^{+2 pi i/1024}; the inverse runs the mirrored steps with conj(w)).
+// Against the 4-pass Stockham schedule (8,4,4,8) this trades one
+// shared-memory exchange and its barrier for 32 shuffles per thread.
+// Output layout: even lanes hold X[t' + 64 r], odd lanes X[t' + 64 r + 512];
+// the Fourier key is produced by the same transform, so the MAC (thread t
+// reads key index t + 128 r) pairs matching frequencies.
+constexpr int FFT1024_HALF = 580;  // odd-parity region offset: 576 (padded 512 points) + 4 slots
+
+template <>
+struct TwiddlesInRegs<1024> {
+    TwiddlesInRegs<512> half;
+    double2 r2[8];  // w^{t' + 64 r}
+    FDSNN_DEV const TwiddlesInRegs<512>& sub() const { return half; }
+    FDSNN_DEV void issue_r2(uint32_t (&)[32]) const {}
+    FDSNN_DEV void finish_r2(uint32_t (&)[32], double2 (&w)[8]) const {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) w[r] = r2[r];
+    }
+};
+
+// TMEM: the 512-point pass twiddles of t' at columns 0-63, w^{t'+64r} at 64-95
+template <>
+struct TwiddlesInTmem<1024> {
+    uint32_t base;
+    FDSNN_DEV TwiddlesInTmem<512> sub() const { return TwiddlesInTmem<512>{base}; }
+    FDSNN_DEV void issue_r2(uint32_t (&raw)[32]) const { tmem_ld32_async(base + 64, raw); }
+    FDSNN_DEV void finish_r2(uint32_t (&raw)[32], double2 (&w)[8]) const {
+        tmem_wait32(raw);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) w[r] = words_c(raw, r);
+    }
+};
+
+FDSNN_DEV double2 shfl_xor1(double2 a) {
+    return make_double2(__shfl_xor_sync(0xffffffffu, a.x, 1), __shfl_xor_sync(0xffffffffu, a.y, 1));
+}
+
+// The radix-2 factor provider returns w^k on odd lanes and 1 on even lanes,
+// so both lanes run the same instructions (no selects): the odd lane
+// pre-multiplies its O by w^k, the lanes swap, and X = partner + s * own with
+// s = +1 (even) / -1 (odd).
+// forward: lanes hold E (even) / O (odd) -> X[k] (even) / X[k+512] (odd)
+template <class TW>
+FDSNN_DEV void r2_join(double2 (&v)[8], int p, const TW& tw) {
+    uint32_t raw[32];
+    tw.issue_r2(raw);
+    double2 w[8];
+    tw.finish_r2(raw, w);
+    const double s = p ? -1.0 : 1.0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const double2 own = cmul(v[r], w[r]);
+        const double2 o = shfl_xor1(own);
+        v[r] = make_double2(fma(s, own.x, o.x), fma(s, own.y, o.y));
+    }
+}
+// inverse: lanes hold X[k] (even) / X[k+512] (odd) -> E' (even) / O' (odd)
+template <class TW>
+FDSNN_DEV void r2_split(double2 (&v)[8], int p, const TW& tw) {
+    uint32_t raw[32];
+    tw.issue_r2(raw);
+    double2 o[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) o[r] = shfl_xor1(v[r]);
+    double2 w[8];
+    tw.finish_r2(raw, w);
+    const double s = p ? -1.0 : 1.0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        v[r] = cmulc(make_double2(fma(s, v[r].x, o[r].x), fma(s, v[r].y, o[r].y)), w[r]);
+}
+
+template <int M, bool INV, class TW, class HOOK = NoHook>
+FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
+                         double2* __restrict__ buf0, double2* __restrict__ buf1,
+                         int& ex, const GroupSync& gs, const HOOK& pre_last = HOOK()) {
+    if constexpr (M == 1024) {
+        const int p = t & 1;
+        double2* b0 = buf0 + p * FFT1024_HALF;
+        double2* b1 = buf1 + p * FFT1024_HALF;
+        if constexpr (INV) {
+            r2_split(v, p, tw);
+            fft_stockham<512, true>(v, t >> 1, tw.sub(), b0, b1, ex, gs, pre_last);
+        } else {
+            fft_stockham<512, false>(v, t >> 1, tw.sub(), b0, b1, ex, gs, pre_last);
+            r2_join(v, p, tw);
+        }
+    } else {
+        fft_stockham<M, INV>(v, t, tw, buf0, buf1, ex, gs, pre_last);
+    }
+}
+
+template <int M, bool INV, class TW, class HOOK = NoHook>
+FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& tw,
+                          double2* __restrict__ buf0, double2* __restrict__ buf1,
+                          const GroupSync& gs, const HOOK& pre_last = HOOK()) {
+    if constexpr (M == 1024) {
+        const int p = t & 1;
+        double2* b0 = buf0 + p * FFT1024_HALF;
+        double2* b1 = buf1 + p * FFT1024_HALF;
+        if constexpr (INV) {
+            r2_split(v0, p, tw);
+            r2_split(v1, p, tw);
+            fft_stockham2<512, true>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
+        } else {
+            fft_stockham2<512, false>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
+            r2_join(v0, p, tw);
+            r2_join(v1, p, tw);
+        }
+    } else {
+        fft_stockham2<M, INV>(v0, v1, t, tw, buf0, buf1, gs, pre_last);
+    }
 }
 
 }  // namespace fdsnn

@@ -59,7 +59,9 @@ struct PbsArgs {
 template <int M>
 struct PbsShape {
     static constexpr int T = M / 8;
-    static constexpr int PADM = M + M / 8;
+    // M = 1024: two 512-point regions, the odd one 4 slots (64 B) further so
+    // that even and odd lanes of a quarter-warp hit different banks
+    static constexpr int PADM = M == 1024 ? FFT1024_HALF + 576 : M + M / 8;
 };
 
 template <int M>
@@ -83,6 +85,51 @@ template <int M>
 FDSNN_DEV void load_twist(double2 (&tw)[8], int t, const double2* __restrict__ tables) {
 #pragma unroll
     for (int r = 0; r < 8; ++r) tw[r] = __ldg(tables + t + r * (M / 8));
+}
+
+// Per-thread transform constants.  M = 1024 (parity split, fft.cuh): the
+// 512-point twiddles of t' = t >> 1 from the M = 512 table, then the radix-2
+// factors w^{t' + 64 r}; host table layout [twist(M) | twiddles | radix-2].
+template <int M>
+FDSNN_DEV void load_tw_regs(TwiddlesInRegs<M>& tw, int t, const double2* __restrict__ tables) {
+    if constexpr (M == 1024) {
+        load_twiddles<512>(tw.half.tw, t >> 1, tables + 1024);
+        const double2* r2 = tables + 1024 + twiddle_table_size<512>();
+#pragma unroll
+        for (int r = 0; r < 8; ++r)  // odd lanes: w^{t' + 64 r}; even lanes: 1 (fft.cuh r2_join)
+            tw.r2[r] = (t & 1) ? __ldg(r2 + (t >> 1) + 64 * r) : make_double2(1.0, 0.0);
+    } else {
+        load_twiddles<M>(tw.tw, t, tables + M);
+    }
+}
+
+FDSNN_DEV void tmem_st_c8(uint32_t col, const double2 (&c)[8]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        double d[8];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) { d[2 * r] = c[4 * h + r].x; d[2 * r + 1] = c[4 * h + r].y; }
+        tmem_st16(col + 16 * h, d);
+    }
+}
+
+// interior-pass twiddles (cols 0..), M = 1024 also the radix-2 factors (64-95)
+template <int M>
+FDSNN_DEV void tmem_store_twiddles(uint32_t lane_base, int t, const double2* __restrict__ tables) {
+    TwiddlesInRegs<M> twr;
+    load_tw_regs<M>(twr, t, tables);
+    constexpr int MS = M == 1024 ? 512 : M;
+    const Twiddles<MS>& tt = [&]() -> const Twiddles<MS>& {
+        if constexpr (M == 1024) return twr.half.tw; else return twr.tw;
+    }();
+#pragma unroll
+    for (int p = 1; p < Schedule<MS>::P; ++p) {
+        double2 c[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) c[r] = tt.w[p][r < 7 ? r : 6];
+        tmem_st_c8(lane_base + (p - 1) * 32, c);
+    }
+    if constexpr (M == 1024) tmem_st_c8(lane_base + 64, twr.r2);
 }
 
 // TMEM columns per lane (256 allocated): interior-pass twiddles of pass p at
@@ -152,22 +199,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
 
     // ---- per-thread constants -> TMEM (warps 0-3 cover all lane quadrants)
     if (warp < 4 && active) {
-        TwiddlesInRegs<M> twr;
-        load_twiddles<M>(twr.tw, t, args.tables + M);
-#pragma unroll
-        for (int p = 1; p < Schedule<M>::P; ++p) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                double d[8];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const double2 w = twr.tw.w[p][4 * h + r < 7 ? 4 * h + r : 6];
-                    d[2 * r] = w.x;
-                    d[2 * r + 1] = w.y;
-                }
-                tmem_st16(lane_base + (p - 1) * 32 + 16 * h, d);
-            }
-        }
+        tmem_store_twiddles<M>(lane_base, t, args.tables);
         double2 twist[8];
         load_twist<M>(twist, t, args.tables);
 #pragma unroll
@@ -736,7 +768,7 @@ bsk_forward_kernel(const int64_t* __restrict__ rows, int64_t npoly, int log2q,
     double2* buf1 = buf0 + PADM;
     const GroupSync gs{1 + g, T};
     TwiddlesInRegs<M> tw;
-    load_twiddles<M>(tw.tw, t, tables + M);
+    load_tw_regs<M>(tw, t, tables);
     const int64_t* src = rows + poly * 2 * M;
     const int64_t qm = (1ll << log2q) - 1;
     double2 vv[8];
