@@ -149,7 +149,7 @@ cudaStream_t pick(fdsnn_ctx* ctx, void* stream) {
 // V = rotations covered by this launch, starting at a.v_base
 template <int M, int G, bool RAW, bool MARGIN, bool PAIR>
 int launch_br_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_t s) {
-    const size_t smem = pbs_smem_bytes<M>(G, 2 * M, ctx->dp.n);
+    const size_t smem = pbs_smem_bytes<M>(G, 2 * M, ctx->dp.n, PAIR && M == 512 && FDSNN_LY2);
     auto kern = pbs_blind_rotate_kernel<M, G, RAW, MARGIN, PAIR>;
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (V + G - 1) / G;
@@ -467,6 +467,16 @@ int fdsnn_ctx_create(const fdsnn_params* prm, int32_t device, fdsnn_ctx** out) {
                     tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
                 }
             ns *= R;
+        }
+        if (M == 512) {  // layout-2 transform twiddles (fft2.cuh): w64^m, w512^m
+            for (int m = 0; m < 64; ++m) {
+                long double ang = 2.0L * PI * m / 64.0L;
+                tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+            }
+            for (int m = 0; m < 512; ++m) {
+                long double ang = 2.0L * PI * m / 512.0L;
+                tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+            }
         }
         if (M == 1024)
             for (int k = 0; k < 512; ++k) {

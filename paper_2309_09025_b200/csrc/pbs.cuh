@@ -31,6 +31,10 @@
 // untwist is a multiply by conj(twist).
 #pragma once
 #include "fft.cuh"
+#include "fft2.cuh"
+#ifndef FDSNN_LY2
+#define FDSNN_LY2 0  // layout-2 transforms (fft2.cuh): bit-exact, 2.5% slower on B200 (DESIGN 8)
+#endif
 
 namespace fdsnn {
 
@@ -64,10 +68,12 @@ struct PbsShape {
     static constexpr int PADM = M == 1024 ? FFT1024_HALF + 576 : M + M / 8;
 };
 
+// LY2 (layout-2 transforms, fft2.cuh): + the warp-local E1 region
+__host__ __device__ constexpr int acc_words(int N, bool) { return N; }
 template <int M>
-__host__ __device__ constexpr size_t pbs_group_bytes(int N, int n) {
-    return 2 * PbsShape<M>::PADM * sizeof(double2)               // exchange buffers
-           + 2 * (size_t)N * sizeof(int32_t)                     // accumulator
+__host__ __device__ constexpr size_t pbs_group_bytes(int N, int n, bool ly2 = false) {
+    return (ly2 ? 3 : 2) * PbsShape<M>::PADM * sizeof(double2)   // exchange buffers
+           + 2 * (size_t)acc_words(N, ly2) * sizeof(int32_t)      // accumulator
            + (((size_t)n * sizeof(uint16_t) + 15) & ~(size_t)15);  // a2N
 }
 
@@ -77,8 +83,8 @@ template <int M>
 __host__ __device__ constexpr size_t pbs_chunk_bytes() { return (size_t)2 * M * sizeof(double2); }
 
 template <int M>
-__host__ __device__ constexpr size_t pbs_smem_bytes(int G, int N, int n) {
-    return 128 + (size_t)PbsRing<M>::S * pbs_chunk_bytes<M>() + (size_t)G * pbs_group_bytes<M>(N, n);
+__host__ __device__ constexpr size_t pbs_smem_bytes(int G, int N, int n, bool ly2 = false) {
+    return 128 + (size_t)PbsRing<M>::S * pbs_chunk_bytes<M>() + (size_t)G * pbs_group_bytes<M>(N, n, ly2);
 }
 
 template <int M>
@@ -152,6 +158,8 @@ template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN, bool PAIR = false>
 __global__ void __launch_bounds__(G * (M / 8), 1)
 pbs_blind_rotate_kernel(const PbsArgs args) {
     constexpr uint32_t TMEM_COLS = PAIR ? 512 : PBS_TMEM_COLS;
+    constexpr bool LY2 = PAIR && M == 512 && FDSNN_LY2;
+    constexpr int NA = acc_words(2 * M, LY2);  // words per accumulator poly
     constexpr int T = M / 8;
     constexpr int PADM = PbsShape<M>::PADM;
     constexpr int S = PbsRing<M>::S;
@@ -171,11 +179,18 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     const int warp = threadIdx.x / 32;
     const int g = threadIdx.x / T;
     const int t = threadIdx.x % T;
-    unsigned char* mine = smem_raw + 128 + S * CHUNK + g * pbs_group_bytes<M>(N, n);
+    unsigned char* mine = smem_raw + 128 + S * CHUNK + g * pbs_group_bytes<M>(N, n, LY2);
     double2* buf0 = reinterpret_cast<double2*>(mine);
     double2* buf1 = buf0 + PADM;
-    int32_t* acc = reinterpret_cast<int32_t*>(buf1 + PADM);  // [2][N]
-    uint16_t* a2N = reinterpret_cast<uint16_t*>(acc + 2 * N);
+    double2* xbuf = buf1 + PADM;  // LY2: warp-local E1 regions (2 x 288)
+    int32_t* acc = reinterpret_cast<int32_t*>(LY2 ? xbuf + PADM : buf1 + PADM);  // [2][NA]
+    uint16_t* a2N = reinterpret_cast<uint16_t*>(acc + 2 * NA);
+    // accumulator word of coefficient j.  LY2 swizzles bit 2 with bit 5: a
+    // warp's layout-2 set {c + 8a + b : a < 8, b < 4} rotated by any k then
+    // hits 32 distinct banks.  The swizzle commutes with adding multiples of
+    // 64, so per-thread offsets r*T + h*M (T = 64) stay compile-time.
+    auto ax = [&](int j) { return LY2 ? j ^ ((j >> 3) & 4) : j; };
+    auto coef = [&](int r, int h) { return (LY2 ? l2::fa_n(t, r) : t + r * T) + h * M; };
 
     const int64_t V = (int64_t)args.nlut * args.count;
     const int64_t v0 = args.v_base + (int64_t)blockIdx.x * G;
@@ -199,9 +214,25 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
 
     // ---- per-thread constants -> TMEM (warps 0-3 cover all lane quadrants)
     if (warp < 4 && active) {
-        tmem_store_twiddles<M>(lane_base, t, args.tables);
         double2 twist[8];
-        load_twist<M>(twist, t, args.tables);
+        if constexpr (LY2) {
+            // w64^(n1 k0) (n1 = 1..7) and w512^(n0 (k0 + 8 k1)) of the fB lane
+            const double2* t64 = args.tables + M + twiddle_table_size<M>();
+            const double2* t512 = t64 + 64;
+            const int k0 = l2::fb_k0(t), n0 = l2::fb_n0(t);
+            double2 c[8];
+#pragma unroll
+            for (int n1 = 0; n1 < 8; ++n1) c[n1] = __ldg(t64 + (((n1 + 1) * k0) & 63));
+            tmem_st_c8(lane_base, c);
+#pragma unroll
+            for (int k1 = 0; k1 < 8; ++k1) c[k1] = __ldg(t512 + ((n0 * (k0 + 8 * k1)) & 511));
+            tmem_st_c8(lane_base + 32, c);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) twist[r] = __ldg(args.tables + l2::fa_n(t, r));
+        } else {
+            tmem_store_twiddles<M>(lane_base, t, args.tables);
+            load_twist<M>(twist, t, args.tables);
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             double d[8];
@@ -256,20 +287,22 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
             const int32_t* lut = args.lut[u];
             // acc_b = X^{-b2N} * v  (monomial_rotate_raw with k = -b2N mod 2N)
             for (int j = t; j < N; j += T) {
-                acc[j] = 0;
+                acc[ax(j)] = 0;
                 const int src = (j + (int)b2N) & (2 * N - 1);
                 const int32_t val = lut[src & (N - 1)];
-                acc[N + j] = (int32_t)((uint32_t)(src >= N ? -val : val) & qmask);
+                acc[NA + ax(j)] = (int32_t)((uint32_t)(src >= N ? -val : val) & qmask);
             }
         } else {
             const int32_t* a_src = args.acc_io + v * 2 * N;
-            for (int j = t; j < 2 * N; j += T) acc[j] = (int32_t)((uint32_t)a_src[j] & qmask);
+            for (int j = t; j < 2 * N; j += T) acc[(j >= N ? NA : 0) + ax(j & (N - 1))] = (int32_t)((uint32_t)a_src[j] & qmask);
             const int32_t* k_src = args.a2N_in + v * n;
             for (int i = t; i < n; i += T) a2N[i] = (uint16_t)(k_src[i] & (2 * N - 1));
         }
         gs.sync();
         const uint32_t own_col = lane_base + PBS_TMEM_OWN + 32 * (uint32_t)(warp / 4);
         const uint32_t o_col = lane_base + 256 + 64 * (uint32_t)(warp / 4);  // PAIR only
+        const uint32_t x_col = lane_base + 384 + 32 * (uint32_t)(warp / 4);  // LY2: E1 TMEM hops
+        const TwiddlesL2 tw2{lane_base};
         {
             uint32_t w[32];
 #pragma unroll
@@ -277,7 +310,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) w[16 * cc + 8 * h + r] = (uint32_t)acc[cc * N + t + r * T + h * M];
+                    for (int r = 0; r < 8; ++r) w[16 * cc + 8 * h + r] = (uint32_t)acc[cc * NA + ax(coef(0, 0)) + r * T + h * M];
             tmem_st32(own_col, w);
             tmem_wait_st();
         }
@@ -316,16 +349,17 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
             // polys are read up front: the second set's shared-memory latency
             // hides behind the first poly's transforms.
             uint32_t rvs[2][16];
+            const int rbase = ax((coef(0, 0) - k) & (2 * N - 1));
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc) {
-                const int32_t* a = acc + cc * N;
+                const int32_t* a = acc + cc * NA;
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {
-                        const int jj = t + r * T + half * M;
-                        const int s = (jj - k) & (2 * N - 1);
-                        rvs[cc][8 * half + r] = (s >= N) ? (uint32_t)(-a[s - N]) : (uint32_t)a[s];
+                        const int s = (rbase + r * T + half * M) & (2 * N - 1);
+                        const uint32_t val = (uint32_t)a[s & (N - 1)];
+                        rvs[cc][8 * half + r] = (s & N) ? (uint32_t)(-val) : val;
                     }
                 }
             }
@@ -363,7 +397,8 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                             v1[r] = cmul(make_double2((double)e1[r], (double)e2[r]), tr);
                         }
                     }
-                    fft_group2<M, false>(v0, v1, t, tw, buf0, buf1, gs);
+                    if constexpr (LY2) fft2_fwd_pair(v0, v1, t, tw2, xbuf, buf0, buf1, x_col, gs);
+                    else fft_group2<M, false>(v0, v1, t, tw, buf0, buf1, gs);
                     const int s0 = (int)(c % S), s1 = (int)((c + 1) % S);
                     mbar_wait(&full[s0], (uint32_t)((c / S) & 1));
                     mbar_wait(&full[s1], (uint32_t)(((c + 1) / S) & 1));
@@ -438,12 +473,13 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
                     tmem_ld32_async(own_col, own);
                 };
-                fft_group2<M, true>(O0, O1, t, tw, buf0, buf1, gs, fetch);
+                if constexpr (LY2) fft2_inv_pair(O0, O1, t, tw2, xbuf, buf0, buf1, x_col, gs, fetch);
+                else fft_group2<M, true>(O0, O1, t, tw, buf0, buf1, gs, fetch);
                 tmem_wait32(twr);
                 tmem_touch32(own);
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
-                    const int p = t + r * T;
+                    const int p = ax(coef(0, 0)) + r * T, pM = p + M;
                     const double2 tr = words_c(twr, r);
                     const double2 z0 = cmulc(O0[r], tr);
                     const double2 z1 = cmulc(O1[r], tr);
@@ -460,9 +496,9 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     own[16 + r] = (own[16 + r] + (uint32_t)r10) & qmask;
                     own[24 + r] = (own[24 + r] + (uint32_t)r11) & qmask;
                     acc[p] = (int32_t)own[r];
-                    acc[p + M] = (int32_t)own[8 + r];
-                    acc[N + p] = (int32_t)own[16 + r];
-                    acc[N + p + M] = (int32_t)own[24 + r];
+                    acc[pM] = (int32_t)own[8 + r];
+                    acc[NA + p] = (int32_t)own[16 + r];
+                    acc[NA + pM] = (int32_t)own[24 + r];
                 }
                 tmem_st32(own_col, own);
                 tmem_wait_st();
@@ -475,15 +511,15 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
 
         if constexpr (MODE_RAW) {
             int32_t* a_dst = args.acc_io + v * 2 * N;
-            for (int j = t; j < 2 * N; j += T) a_dst[j] = acc[j];
+            for (int j = t; j < 2 * N; j += T) a_dst[j] = acc[(j >= N ? NA : 0) + ax(j & (N - 1))];
         } else {
             // sample extract (bootstrap.py:484-488): (a_0, -a_{N-1}, ..., -a_1), b = acc_b[0]
             uint32_t* out = args.ext_out + v * prm.ext_stride;
             for (int j = t; j < N; j += T) {
-                const uint32_t a = (j == 0) ? (uint32_t)acc[0] : ((uint32_t)(-acc[N - j]) & qmask);
+                const uint32_t a = (j == 0) ? (uint32_t)acc[0] : ((uint32_t)(-acc[ax(N - j)]) & qmask);
                 out[j] = a;
             }
-            if (t == 0) out[N] = (uint32_t)acc[N];
+            if (t == 0) out[N] = (uint32_t)acc[NA];
         }
     }  // active
     tmem_fence_before();
