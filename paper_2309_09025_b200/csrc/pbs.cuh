@@ -78,7 +78,11 @@ __host__ __device__ constexpr size_t pbs_group_bytes(int N, int n, bool ly2 = fa
 }
 
 constexpr int PBS_THREADS = 256;
-template <int M> struct PbsRing { static constexpr int S = (M == 1024) ? 3 : 4; };
+#ifndef FDSNN_RING_S
+#define FDSNN_RING_S 4
+#endif
+template <int M> struct PbsRing { static constexpr int S = (M == 1024) ? 3 : FDSNN_RING_S; };
+static_assert(FDSNN_RING_S >= 2 && FDSNN_RING_S <= 7, "mbarriers live in the 120-byte ring header");
 template <int M>
 __host__ __device__ constexpr size_t pbs_chunk_bytes() { return (size_t)2 * M * sizeof(double2); }
 
@@ -173,7 +177,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);   // key chunk landed
-    uint64_t* empty = full + 4;                                // ring stage free
+    uint64_t* empty = full + S;                                // ring stage free (2S <= 15 slots)
     uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem_raw + 120);
     double2* ring = reinterpret_cast<double2*>(smem_raw + 128);
     const int warp = threadIdx.x / 32;
@@ -545,8 +549,7 @@ __global__ void __launch_bounds__(L2 * (M / 8), 1)
 pbs_blind_rotate_wide_kernel(const PbsArgs args) {
     constexpr int T = M / 8;
     constexpr int PADM = PbsShape<M>::PADM;
-    constexpr int S = PbsRing<M>::S;
-    static_assert(L2 == S, "one ring stage per digit of a step");
+    constexpr int S = L2;  // one ring stage per digit of a step
     constexpr uint32_t CHUNK = (uint32_t)pbs_chunk_bytes<M>();
     constexpr int NT = L2 * T;
     const DevParams& prm = args.prm;
@@ -558,7 +561,7 @@ pbs_blind_rotate_wide_kernel(const PbsArgs args) {
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-    uint64_t* empty = full + 4;
+    uint64_t* empty = full + S;
     uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem_raw + 120);
     double2* ring = reinterpret_cast<double2*>(smem_raw + 128);
     const int warp = threadIdx.x / 32;
@@ -782,7 +785,7 @@ pbs_blind_rotate_wide_kernel(const PbsArgs args) {
 
 template <int M>
 __host__ __device__ constexpr size_t pbs_wide_smem_bytes(int L2, int N, int n) {
-    return 128 + (size_t)PbsRing<M>::S * pbs_chunk_bytes<M>() + (size_t)L2 * 2 * PbsShape<M>::PADM * sizeof(double2) +
+    return 128 + (size_t)L2 * pbs_chunk_bytes<M>() + (size_t)L2 * 2 * PbsShape<M>::PADM * sizeof(double2) +
            2 * (size_t)N * sizeof(int32_t) + (((size_t)n * sizeof(uint16_t) + 15) & ~(size_t)15);
 }
 
