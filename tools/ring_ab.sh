@@ -1,9 +1,10 @@
-# Timing ablation (dev aid, results invalid): refill 1/2 or 1/16 of each key chunk
+# A/B of the key-ring depth (dev aid): FDSNN_RING_S = 3, 4 (default), 5
 cd $GRAFT_REPO_ROOT
 B=paper_2309_09025_b200
-cp $B/libfdsnn_b200.so /tmp/base.so
-for v in base tools/abl_k2 tools/abl_k16 base; do
-  if [ $v = base ]; then cp /tmp/base.so $B/libfdsnn_b200.so; else cp $v.so $B/libfdsnn_b200.so; fi
-  echo "$v"; timeout 300 python tools/perf_probe.py 2048 8192 2>&1 | tail -2
+cp $B/libfdsnn_b200.so /tmp/s4.so
+for S in 3 5; do
+  (cd $B/csrc && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -shared -Xcompiler -fPIC \
+      -diag-suppress 177,1886 -DFDSNN_RING_S=$S -o /tmp/s$S.so capi.cu)
 done
-cp /tmp/base.so $B/libfdsnn_b200.so
+for S in 4 3 5 4; do cp /tmp/s$S.so $B/libfdsnn_b200.so; echo "S=$S"; timeout 300 python tools/perf_probe.py 2048 8192 2>&1 | tail -2; done
+cp /tmp/s4.so $B/libfdsnn_b200.so
