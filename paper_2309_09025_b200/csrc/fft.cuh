@@ -298,6 +298,58 @@ FDSNN_DEV void fft_stockham2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW
 #undef FDSNN_FFT2_STEP
 }
 
+// Software-pipelined pair: v1 runs half an exchange behind v0, so each batch
+// of exchange loads is followed by the other transform's butterflies (which
+// hide the load latency) instead of by its own consumer.  Each barrier is the
+// read-after-write fence of one buffer and the write-after-read fence of the
+// other: 2P-1 barriers per pair against 2(P-1) for fft_stockham2.
+template <int M, bool INV, class TW, class HOOK = NoHook>
+FDSNN_DEV void fft_stockham2p(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& tw,
+                              double2* __restrict__ buf0, double2* __restrict__ buf1,
+                              const GroupSync& gs, const HOOK& pre_last = HOOK()) {
+    constexpr int P = Schedule<M>::P;
+    static_assert(P == 3, "pipelined pair written for three passes");
+    {
+        double2 w[8];
+        pass_body<M, 0, INV>(v0, w);
+        gs.sync();  // previous readers of both buffers are done
+        pass_store<M, 0>(v0, t, buf0);
+        gs.sync();
+        pass_load<M, 1>(v0, t, buf0);
+        pass_body<M, 0, INV>(v1, w);
+    }
+    {
+        uint32_t raw[32];
+        tw.template issue<1>(raw);
+        pass_store<M, 0>(v1, t, buf1);
+        double2 w[8];
+        tw.template finish<1>(raw, w);
+        gs.sync();
+        pass_load<M, 1>(v1, t, buf1);
+        pass_body<M, 1, INV>(v0, w);
+        pass_store<M, 1>(v0, t, buf0);
+        gs.sync();
+        pass_load<M, 2>(v0, t, buf0);
+        pass_body<M, 1, INV>(v1, w);
+    }
+    {
+        uint32_t raw[32];
+        tw.template issue<2>(raw);
+        pass_store<M, 1>(v1, t, buf1);
+        double2 w[8];
+        tw.template finish<2>(raw, w);
+        gs.sync();
+        pass_load<M, 2>(v1, t, buf1);
+        pre_last();
+        pass_body<M, 2, INV>(v0, w);
+        pass_body<M, 2, INV>(v1, w);
+    }
+}
+
+#ifndef FDSNN_PIPE2
+#define FDSNN_PIPE2 1
+#endif
+
 // ---------------------------------------------------------------------------
 // M = 1024 as a parity split (C4, N = 2048): thread t = 2t' + p holds the
 // points {t + 128 r} = {2(t' + 64 r) + p}, i.e. the 512-point subsequence of
@@ -415,6 +467,8 @@ FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& t
             r2_join(v0, p, tw);
             r2_join(v1, p, tw);
         }
+    } else if constexpr (FDSNN_PIPE2 && Schedule<M>::P == 3) {
+        fft_stockham2p<M, INV>(v0, v1, t, tw, buf0, buf1, gs, pre_last);
     } else {
         fft_stockham2<M, INV>(v0, v1, t, tw, buf0, buf1, gs, pre_last);
     }

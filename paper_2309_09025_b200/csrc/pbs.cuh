@@ -86,9 +86,12 @@ static_assert(FDSNN_RING_S >= 2 && FDSNN_RING_S <= 7, "mbarriers live in the 120
 template <int M>
 __host__ __device__ constexpr size_t pbs_chunk_bytes() { return (size_t)2 * M * sizeof(double2); }
 
+// 6 rotations per CTA (12 warps) leave room for only 3 ring stages
+template <int M>
+__host__ __device__ constexpr int pbs_stages(int G) { return G >= 6 ? 3 : PbsRing<M>::S; }
 template <int M>
 __host__ __device__ constexpr size_t pbs_smem_bytes(int G, int N, int n, bool ly2 = false) {
-    return 128 + (size_t)PbsRing<M>::S * pbs_chunk_bytes<M>() + (size_t)G * pbs_group_bytes<M>(N, n, ly2);
+    return 128 + (size_t)pbs_stages<M>(G) * pbs_chunk_bytes<M>() + (size_t)G * pbs_group_bytes<M>(N, n, ly2);
 }
 
 template <int M>
@@ -166,7 +169,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     constexpr int NA = acc_words(2 * M, LY2);  // words per accumulator poly
     constexpr int T = M / 8;
     constexpr int PADM = PbsShape<M>::PADM;
-    constexpr int S = PbsRing<M>::S;
+    constexpr int S = pbs_stages<M>(G);
     constexpr uint32_t CHUNK = (uint32_t)pbs_chunk_bytes<M>();
     const DevParams& prm = args.prm;
     constexpr int N = 2 * M;
