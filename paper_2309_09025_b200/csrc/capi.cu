@@ -194,8 +194,6 @@ int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_
                 int64_t rem = V % round4, full = V - rem;
                 if (rem > 3 * sms) { full = V; rem = 0; }
                 ts.kernels = (full > 0) + (rem > 0);
-                static const bool g6 = getenv("FDSNN_G6") && atoi(getenv("FDSNN_G6")) == 1;
-                if (g6) return launch_br_m<512, 6, true>(ctx, a, V, raw, s);
                 if (full > 0) {
                     int rc = launch_br_m<512, 4, true>(ctx, a, full, raw, s);
                     if (rc) return rc;
