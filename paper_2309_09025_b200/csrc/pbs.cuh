@@ -32,6 +32,9 @@
 #pragma once
 #include "fft.cuh"
 #include "fft2.cuh"
+#ifndef FDSNN_EARLY_KEYS
+#define FDSNN_EARLY_KEYS 1
+#endif
 #ifndef FDSNN_LY2
 #define FDSNN_LY2 0  // layout-2 transforms (fft2.cuh): bit-exact, 2.5% slower on B200 (DESIGN 8)
 #endif
@@ -404,11 +407,22 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                             v1[r] = cmul(make_double2((double)e1[r], (double)e2[r]), tr);
                         }
                     }
-                    if constexpr (LY2) fft2_fwd_pair(v0, v1, t, tw2, xbuf, buf0, buf1, x_col, gs);
-                    else fft_group2<M, false>(v0, v1, t, tw, buf0, buf1, gs);
                     const int s0 = (int)(c % S), s1 = (int)((c + 1) % S);
-                    mbar_wait(&full[s0], (uint32_t)((c / S) & 1));
-                    mbar_wait(&full[s1], (uint32_t)(((c + 1) / S) & 1));
+                    // key chunks landed: waited for before the last pass, so
+                    // the MAC's key loads may be scheduled into it
+                    auto keys_ready = [&]() {
+                        mbar_wait(&full[s0], (uint32_t)((c / S) & 1));
+                        mbar_wait(&full[s1], (uint32_t)(((c + 1) / S) & 1));
+                    };
+                    if constexpr (LY2) {
+                        fft2_fwd_pair(v0, v1, t, tw2, xbuf, buf0, buf1, x_col, gs);
+                        keys_ready();
+                    } else if constexpr (FDSNN_EARLY_KEYS) {
+                        fft_group2<M, false>(v0, v1, t, tw, buf0, buf1, gs, keys_ready);
+                    } else {
+                        fft_group2<M, false>(v0, v1, t, tw, buf0, buf1, gs);
+                        keys_ready();
+                    }
                     const double2* k0 = ring + (size_t)s0 * 2 * M;
                     const double2* k1 = ring + (size_t)s1 * 2 * M;
                     if (cc == 0) {
