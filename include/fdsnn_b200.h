@@ -193,6 +193,29 @@ int fdsnn_timing_reset(fdsnn_ctx* ctx);
 int fdsnn_margin_enable(fdsnn_ctx* ctx, int32_t on);
 int fdsnn_margin_read(fdsnn_ctx* ctx, double* max_err);
 
+/* ---- ring / RGSW algebra (host buffers, synchronous, no context) ------
+ * The reference's algebra layer for users outside the bootstrapping path
+ * (tests, key tooling).  `device` selects the GPU; arrays are host memory.
+ * ring.NegacyclicTransform.forward (ring.py:125-131): count real length-N
+ * polynomials (float64) -> count x N/2 complex evaluations, interleaved
+ * (re, im) float64.  N a power of two in [2, 4096]. */
+int fdsnn_nt_forward(int32_t device, int32_t N, const double* coeffs, double* evals, int64_t count);
+/* ring.NegacyclicTransform.inverse (ring.py:133-137): unrounded coefficients. */
+int fdsnn_nt_inverse(int32_t device, int32_t N, const double* evals, double* coeffs, int64_t count);
+/* Exact negacyclic multiply-accumulate mod q = 2^log2_q, replacing
+ * ring.poly_mul / poly_mul_schoolbook / negacyclic_mul_raw (ring.py:200-223)
+ * and the MAC of rgsw.external_product (rgsw.py:189-192):
+ * out[b] = sum_{d<D} x[b][d] * y[b][d] mod (X^N + 1, q); x, y (count, D, N)
+ * int64 (any representatives), out (count, N) in [0, q).  Exact at every
+ * size (the reference's transform path is exact only while N max|x| max|y|
+ * stays below 2^53; where it is, the results are identical). */
+int fdsnn_negacyclic_mac(int32_t device, int32_t N, int32_t log2_q, int32_t D, const int64_t* x,
+                         const int64_t* y, int64_t* out, int64_t count);
+/* rgsw.gadget_decompose (rgsw.py:119-133): signed digits in (-B/2, B/2],
+ * lowest level first; x (rows, len) -> digits (rows, levels, len). */
+int fdsnn_gadget_decompose(int32_t device, int32_t log2_q, int32_t bg_log, int32_t levels, const int64_t* x,
+                           int64_t rows, int64_t len, int64_t* digits);
+
 /* Microbenchmarks for the roofline denominators (run on ctx's device). */
 int fdsnn_probe_fp64_peak(fdsnn_ctx* ctx, double* tflops);
 int fdsnn_flush_l2(fdsnn_ctx* ctx, void* stream);

@@ -93,6 +93,29 @@ def gadget_decompose(x, q, base, levels):
     return out
 
 
+def negacyclic_mul(a, b, q):
+    """Exact a*b mod (X^N + 1, q) of integer vectors (ring.py:200-207 schoolbook;
+    the reference's transform path ring.py:210-223 equals it at preset sizes).
+    int64 convolution: exact while N*max|a|*max|b| < 2^63."""
+    a = center(np.asarray(a, dtype=np.int64) % q, q)
+    b = np.asarray(b, dtype=np.int64)
+    N = a.shape[-1]
+    full = np.convolve(a, b)
+    out = full[:N].copy()
+    out[: len(full) - N] -= full[N:]
+    return out % q
+
+
+def external_product(ct_a, ct_b, rows_a, rows_b, q, base, levels):
+    """RLWE x RGSW (rgsw.py:179-193): digits of (a, b) stacked (2l, N), then
+    sum_d digit_d * row_d for the a and the b component, mod q."""
+    digits = np.concatenate([gadget_decompose(np.asarray(ct_a)[None], q, base, levels)[0],
+                             gadget_decompose(np.asarray(ct_b)[None], q, base, levels)[0]])
+    out_a = sum(negacyclic_mul(r, d, q) for r, d in zip(rows_a, digits)) % q
+    out_b = sum(negacyclic_mul(r, d, q) for r, d in zip(rows_b, digits)) % q
+    return out_a, out_b
+
+
 # --------------------------------------------------------- bootstrap.py
 
 

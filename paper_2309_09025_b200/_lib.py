@@ -73,6 +73,10 @@ SIGNATURES = {
     "fdsnn_margin_read": (_c_int, [_vp, _dp]),
     "fdsnn_probe_fp64_peak": (_c_int, [_vp, _dp]),
     "fdsnn_flush_l2": (_c_int, [_vp, _vp]),
+    "fdsnn_nt_forward": (_c_int, [_i32, _i32, _vp, _vp, _i64]),
+    "fdsnn_nt_inverse": (_c_int, [_i32, _i32, _vp, _vp, _i64]),
+    "fdsnn_negacyclic_mac": (_c_int, [_i32, _i32, _i32, _i32, _vp, _vp, _vp, _i64]),
+    "fdsnn_gadget_decompose": (_c_int, [_i32, _i32, _i32, _i32, _vp, _i64, _i64, _vp]),
 }
 
 _lib = None

@@ -22,6 +22,7 @@
 #include "pbs.cuh"
 #include "plain.cuh"
 #include "lwe_dev.cuh"
+#include "ring_ops.cuh"
 
 using namespace fdsnn;
 
@@ -1103,3 +1104,108 @@ int fdsnn_flush_l2(fdsnn_ctx* ctx, void* stream) {
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// Ring / RGSW algebra (host buffers, one device, synchronous): the reference's
+// ring.NegacyclicTransform, poly_mul(_schoolbook), rgsw.gadget_decompose.
+// ===========================================================================
+namespace {
+struct DevScratch {
+    void* p = nullptr;
+    ~DevScratch() { if (p) cudaFree(p); }
+};
+
+int ring_device(int32_t device) {
+    int n = 0;
+    CU(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return set_err(FDSNN_ERR_PARAMETER, "no CUDA device %d", device);
+    CU(cudaSetDevice(device));
+    return FDSNN_OK;
+}
+
+template <bool INV>
+int nt_run(int32_t device, int32_t N, const double* in, double* out, int64_t count) {
+    if (!is_pow2(N) || N < 2 || N > 4096)
+        return set_err(FDSNN_ERR_PARAMETER, "negacyclic transform: N=%d must be a power of two in [2, 4096]", N);
+    if (count < 0 || (count > 0 && (!in || !out))) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
+    if (count == 0) return FDSNN_OK;
+    if (int rc = ring_device(device)) return rc;
+    const size_t bytes = (size_t)count * N * sizeof(double);  // N reals == N/2 complex
+    DevScratch din, dout;
+    CU(cudaMalloc(&din.p, bytes));
+    CU(cudaMalloc(&dout.p, bytes));
+    CU(cudaMemcpy(din.p, in, bytes, cudaMemcpyHostToDevice));
+    const size_t smem = (size_t)(N / 2) * sizeof(double2);
+    CU(cudaFuncSetAttribute(nt_fft_kernel<INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int threads = N / 4 < 32 ? 32 : (N / 4 > 512 ? 512 : N / 4);
+    for (int64_t b0 = 0; b0 < count; b0 += 65535) {
+        const int64_t nb = count - b0 < 65535 ? count - b0 : 65535;
+        nt_fft_kernel<INV><<<(unsigned)nb, threads, smem>>>(N, (const double*)din.p + b0 * N, (double*)dout.p + b0 * N);
+        CU(cudaGetLastError());
+    }
+    CU(cudaMemcpy(out, dout.p, bytes, cudaMemcpyDeviceToHost));
+    return FDSNN_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int fdsnn_nt_forward(int32_t device, int32_t N, const double* coeffs, double* evals, int64_t count) {
+    return nt_run<false>(device, N, coeffs, evals, count);
+}
+
+int fdsnn_nt_inverse(int32_t device, int32_t N, const double* evals, double* coeffs, int64_t count) {
+    return nt_run<true>(device, N, evals, coeffs, count);
+}
+
+int fdsnn_negacyclic_mac(int32_t device, int32_t N, int32_t log2_q, int32_t D, const int64_t* x,
+                         const int64_t* y, int64_t* out, int64_t count) {
+    if (!is_pow2(N) || N > 4096) return set_err(FDSNN_ERR_PARAMETER, "negacyclic product: N=%d unsupported", N);
+    if (log2_q < 1 || log2_q > 63) return set_err(FDSNN_ERR_PARAMETER, "q must be 2^1..2^63");
+    if (D < 1 || count < 0 || (count > 0 && (!x || !y || !out))) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
+    if (count == 0) return FDSNN_OK;
+    if (int rc = ring_device(device)) return rc;
+    const size_t in_bytes = (size_t)count * D * N * sizeof(int64_t), out_bytes = (size_t)count * N * sizeof(int64_t);
+    DevScratch dx, dy, dout;
+    CU(cudaMalloc(&dx.p, in_bytes));
+    CU(cudaMalloc(&dy.p, in_bytes));
+    CU(cudaMalloc(&dout.p, out_bytes));
+    CU(cudaMemcpy(dx.p, x, in_bytes, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dy.p, y, in_bytes, cudaMemcpyHostToDevice));
+    const int threads = N < 256 ? (N < 32 ? 32 : N) : 256;
+    const size_t smem = 2 * (size_t)N * sizeof(uint64_t);
+    CU(cudaFuncSetAttribute(negacyclic_mac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const uint64_t qmask = (1ull << log2_q) - 1;
+    for (int64_t b0 = 0; b0 < count; b0 += 65535) {
+        const int64_t nb = count - b0 < 65535 ? count - b0 : 65535;
+        dim3 grid((unsigned)nb, (unsigned)((N + threads - 1) / threads));
+        negacyclic_mac_kernel<<<grid, threads, smem>>>(N, qmask, D, (const int64_t*)dx.p + b0 * D * N,
+                                                      (const int64_t*)dy.p + b0 * D * N,
+                                                      (int64_t*)dout.p + b0 * N);
+        CU(cudaGetLastError());
+    }
+    CU(cudaMemcpy(out, dout.p, out_bytes, cudaMemcpyDeviceToHost));
+    return FDSNN_OK;
+}
+
+int fdsnn_gadget_decompose(int32_t device, int32_t log2_q, int32_t bg_log, int32_t levels, const int64_t* x,
+                           int64_t rows, int64_t len, int64_t* digits) {
+    if (log2_q < 1 || log2_q > 62 || bg_log < 1 || levels < 1 || (int64_t)bg_log * levels > 63)
+        return set_err(FDSNN_ERR_PARAMETER, "gadget: q=2^%d, B=2^%d, levels=%d unsupported", log2_q, bg_log, levels);
+    if (rows < 0 || len < 0 || (rows * len > 0 && (!x || !digits))) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
+    if (rows * len == 0) return FDSNN_OK;
+    if (int rc = ring_device(device)) return rc;
+    const size_t in_bytes = (size_t)rows * len * sizeof(int64_t);
+    DevScratch dx, dd;
+    CU(cudaMalloc(&dx.p, in_bytes));
+    CU(cudaMalloc(&dd.p, in_bytes * levels));
+    CU(cudaMemcpy(dx.p, x, in_bytes, cudaMemcpyHostToDevice));
+    gadget_digits_kernel<<<grid1d(rows * len), 256>>>(log2_q, bg_log, levels, (const int64_t*)dx.p, rows, len,
+                                                     (int64_t*)dd.p);
+    CU(cudaGetLastError());
+    CU(cudaMemcpy(digits, dd.p, in_bytes * levels, cudaMemcpyDeviceToHost));
+    return FDSNN_OK;
+}
+
+}  // extern "C"
+

@@ -1,17 +1,24 @@
 """Host-side integer helpers for Z_q and Z_q[X]/(X^N+1) (reference ring.py).
 
 These are the rounding rules the device kernels reproduce bit for bit
-(round-half-away on centred representatives, ring.py:27-67) plus the small
-host utilities the key generator needs.  Nothing here is on the accelerated
-path: ciphertext-batch work goes through the CUDA library.
+(round-half-away on centred representatives, ring.py:27-67), the small host
+utilities the key generator needs (`negacyclic_mul_raw` for RLWE bodies,
+`monomial_rotate_raw` for test polynomials) and the value types
+(`ZqElement`, `NegacyclicPoly`).  The algebra API that does real polynomial
+arithmetic -- `NegacyclicTransform`, `poly_mul`, `poly_mul_schoolbook` --
+runs on the GPU through the C library (csrc/ring_ops.cuh) and, like every
+compute path of this package, has no CPU fallback.
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
+from functools import lru_cache
 
 import numpy as np
 
+from . import _lib
 from .errors import ParameterError
 
 
@@ -109,3 +116,160 @@ class NegacyclicPoly:
         coeffs = np.zeros(N, dtype=np.int64)
         coeffs[0] = c % q
         return NegacyclicPoly(coeffs, q)
+
+    @staticmethod
+    def zero(N: int, q: int) -> "NegacyclicPoly":
+        return NegacyclicPoly(np.zeros(N, dtype=np.int64), q)
+
+    def _check(self, other: "NegacyclicPoly") -> None:
+        if self.q != other.q or self.N != other.N:
+            raise ParameterError("ring parameters mismatch")
+
+    def __add__(self, other: "NegacyclicPoly") -> "NegacyclicPoly":
+        self._check(other)
+        return NegacyclicPoly(self.coeffs + other.coeffs, self.q)
+
+    def __sub__(self, other: "NegacyclicPoly") -> "NegacyclicPoly":
+        self._check(other)
+        return NegacyclicPoly(self.coeffs - other.coeffs, self.q)
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, NegacyclicPoly) and self.q == other.q
+                and np.array_equal(self.coeffs, other.coeffs))
+
+    __hash__ = None
+
+
+@dataclass(frozen=True)
+class ZqElement:
+    """Scalar of Z_q, q a power of two (ring.py:71-100)."""
+
+    value: int
+    q: int
+
+    def __post_init__(self):
+        if not is_power_of_two(self.q):
+            raise ParameterError("q must be a power of two")
+        object.__setattr__(self, "value", int(self.value) % self.q)
+
+    @property
+    def centered(self) -> int:
+        return center(self.value, self.q)
+
+    def _same(self, other: "ZqElement") -> None:
+        if self.q != other.q:
+            raise ParameterError("modulus mismatch")
+
+    def __add__(self, other: "ZqElement") -> "ZqElement":
+        self._same(other)
+        return ZqElement(self.value + other.value, self.q)
+
+    def __sub__(self, other: "ZqElement") -> "ZqElement":
+        self._same(other)
+        return ZqElement(self.value - other.value, self.q)
+
+    def __mul__(self, other: "ZqElement") -> "ZqElement":
+        self._same(other)
+        return ZqElement(self.value * other.value, self.q)
+
+
+def monomial_rotate(p: NegacyclicPoly, k: int) -> NegacyclicPoly:
+    """X^k * p with the X^N = -1 sign wrap, k modulo 2N (ring.py:245-247)."""
+    return NegacyclicPoly(monomial_rotate_raw(p.coeffs, int(k), p.N), p.q)
+
+
+# --------------------------------------------------------------------------
+# device algebra (csrc/ring_ops.cuh)
+# --------------------------------------------------------------------------
+def _dev() -> int:
+    import torch  # noqa: F401  (device index of the current torch device, if any)
+    return int(torch.cuda.current_device()) if torch.cuda.is_available() else 0
+
+
+def _f64(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+
+
+class NegacyclicTransform:
+    """Length-N negacyclic transform through a half-size complex DFT
+    (ring.py:103-137), evaluated on the GPU.
+
+    forward: c_k = (a_k + i a_{k+N/2}) e^{i pi k/N}, then the unnormalised
+    N/2-point DFT with the e^{+2 pi i jk/(N/2)} kernel; inverse: the e^{-}
+    DFT divided by N/2, times e^{-i pi k/N}, real parts then imaginary parts
+    (unrounded).  FP64 throughout; agrees with the reference's pocketfft
+    transform to rounding (tests/test_gpu_ring.py).
+    """
+
+    def __init__(self, N: int):
+        if not is_power_of_two(N) or N < 2:
+            raise ParameterError("N must be a power of two >= 2")
+        if N > 4096:
+            raise ParameterError("device negacyclic transform supports N <= 4096")
+        self.N = N
+        k = np.arange(N // 2)
+        self.twist = np.exp(1j * np.pi * k / N)
+        self.untwist = np.conj(self.twist)
+
+    def forward(self, coeffs: np.ndarray) -> np.ndarray:
+        """(..., N) int/float -> (..., N/2) complex evaluations."""
+        a = _f64(coeffs)
+        if a.shape[-1] != self.N:
+            raise ParameterError(f"expected trailing length {self.N}")
+        lead = a.shape[:-1]
+        out = np.empty(lead + (self.N,), dtype=np.float64)  # N/2 interleaved complex
+        lib = _lib.load()
+        _lib.check(lib.fdsnn_nt_forward(_dev(), self.N, ctypes.c_void_p(a.ctypes.data),
+                                        ctypes.c_void_p(out.ctypes.data), int(np.prod(lead, dtype=np.int64))))
+        return out.view(np.complex128)
+
+    def inverse(self, evals: np.ndarray) -> np.ndarray:
+        """(..., N/2) complex -> (..., N) float coefficients (unrounded)."""
+        e = np.ascontiguousarray(np.asarray(evals, dtype=np.complex128))
+        if e.shape[-1] != self.N // 2:
+            raise ParameterError(f"expected trailing length {self.N // 2}")
+        lead = e.shape[:-1]
+        out = np.empty(lead + (self.N,), dtype=np.float64)
+        lib = _lib.load()
+        _lib.check(lib.fdsnn_nt_inverse(_dev(), self.N, ctypes.c_void_p(e.ctypes.data),
+                                        ctypes.c_void_p(out.ctypes.data), int(np.prod(lead, dtype=np.int64))))
+        return out
+
+
+@lru_cache(maxsize=None)
+def get_transform(N: int) -> NegacyclicTransform:
+    return NegacyclicTransform(N)
+
+
+def negacyclic_mac_device(x: np.ndarray, y: np.ndarray, q: int) -> np.ndarray:
+    """sum_d x[..., d, :] * y[..., d, :] mod (X^N + 1, q), exact, on the GPU.
+
+    x, y (..., D, N) int64 (any representatives) -> (..., N) in [0, q)."""
+    if not is_power_of_two(q):
+        raise ParameterError("q must be a power of two")
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.int64))
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.int64))
+    if x.shape != y.shape or x.ndim < 2:
+        raise ParameterError("operand shapes differ")
+    D, N = x.shape[-2:]
+    lead = x.shape[:-2]
+    out = np.empty(lead + (N,), dtype=np.int64)
+    lib = _lib.load()
+    _lib.check(lib.fdsnn_negacyclic_mac(_dev(), N, q.bit_length() - 1, D, ctypes.c_void_p(x.ctypes.data),
+                                        ctypes.c_void_p(y.ctypes.data), ctypes.c_void_p(out.ctypes.data),
+                                        int(np.prod(lead, dtype=np.int64))))
+    return out
+
+
+def poly_mul_schoolbook(a: NegacyclicPoly, b: NegacyclicPoly) -> NegacyclicPoly:
+    """Exact negacyclic product (ring.py:200-207), computed on the GPU."""
+    a._check(b)
+    return NegacyclicPoly(negacyclic_mac_device(a.coeffs[None], b.coeffs[None], a.q), a.q)
+
+
+def poly_mul(a: NegacyclicPoly, b: NegacyclicPoly) -> NegacyclicPoly:
+    """Negacyclic product (ring.py:218-223).  The reference's transform path
+    is exact at the preset sizes; the device computes the exact product
+    directly, so the results are identical there and exact everywhere."""
+    return poly_mul_schoolbook(a, b)
+

@@ -8,7 +8,7 @@ reference.  Run:
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
         python tests/golden/make_golden.py [section ...]
 
-Sections: keys toy toy64 desk c4 layer config0 config1 config2 fdsn plain paper
+Sections: keys toy toy64 desk c4 layer config0 config1 config2 fdsn plain paper ring
 """
 
 from __future__ import annotations
@@ -312,13 +312,52 @@ def sec_fdsn():
     print("wrote fdsn.json")
 
 
+def sec_ring():
+    """Algebra layer: negacyclic transform, products, digits, external product."""
+    from fdsnn import params as P, rgsw, ring
+    rng = np.random.default_rng(61)
+    out = {}
+    for N in (2, 8, 64, 1024, 2048):
+        a = rng.integers(-(1 << 24), 1 << 24, (2 if N < 1024 else 1, N))
+        tr = ring.NegacyclicTransform(N)
+        f = tr.forward(a)
+        out[f"nt{N}_in"], out[f"nt{N}_fwd"], out[f"nt{N}_inv"] = a, f, tr.inverse(f)
+    for name, N, q, bmax in (("desk", 1024, 1 << 25, 1 << 12), ("c4", 2048, 1 << 24, 1 << 7), ("tiny", 8, 1 << 12, 1 << 12)):
+        a = rng.integers(0, q, N)
+        b = rng.integers(-bmax, bmax + 1, N)
+        pa, pb = ring.NegacyclicPoly(a, q), ring.NegacyclicPoly(b, q)
+        out[f"mul_{name}_a"], out[f"mul_{name}_b"] = a, b
+        out[f"mul_{name}_q"] = np.array([q])
+        out[f"mul_{name}_out"] = ring.poly_mul(pa, pb).coeffs
+    for name, q, base, levels in (("desk", 1 << 25, 1 << 13, 2), ("c4", 1 << 24, 1 << 8, 3), ("small", 1 << 12, 1 << 6, 2)):
+        x = np.concatenate([rng.integers(0, q, 4000), [0, 1, q - 1, q // 2, q // 2 - 1, q // 2 + 1]])
+        out[f"dig_{name}_x"] = x
+        out[f"dig_{name}_prm"] = np.array([q, base, levels])
+        out[f"dig_{name}_out"] = rgsw.gadget_decompose(x, q, P.GadgetParams(base=base, levels=levels))
+    small = P.FheParams(n=4, q=1 << 12, N=64, p=8, sigma=1e-9, gadget=P.GadgetParams(base=1 << 6, levels=2),
+                        ks_base=8, ks_levels=4, sigma_bk=1e-9, sigma_ks=1e-9)
+    for name, prm, k in (("small", small, 37), ("desk", W.desk1024(fdsnn), 700)):
+        erng = np.random.default_rng(62)
+        zk = rgsw.rlwe_keygen(prm, erng)
+        m = ring.NegacyclicPoly(erng.integers(0, prm.p, prm.N), prm.p)
+        ct = rgsw.rlwe_encrypt(m, zk, prm, erng)
+        g = rgsw.rgsw_encrypt_monomial(k, zk, prm, erng)
+        res = rgsw.external_product(ct, g, prm)
+        out[f"ext_{name}_ct"] = np.stack([ct.a, ct.b])
+        out[f"ext_{name}_rows"] = np.stack([g.rows_a, g.rows_b])
+        out[f"ext_{name}_gadget"] = np.array([prm.q, prm.gadget.base, prm.gadget.levels, prm.N])
+        out[f"ext_{name}_out"] = np.stack([res.a, res.b])
+        out[f"ext_{name}_z"] = zk.z
+    save("ring", **out)
+
+
 SECTIONS = {
     "fdsn": sec_fdsn,
     "keys": sec_keys, "toy": sec_toy, "toy64": sec_toy64,
     "desk": lambda: sec_lif(W.desk1024(fdsnn), "desk_lif", 32),
     "c4": lambda: sec_lif(W.c4_params(fdsnn), "c4_lif", 4),
     "layer": sec_layer, "config0": sec_config0, "config1": sec_config1, "config2": sec_config2,
-    "plain": sec_plain, "paper": sec_paper,
+    "plain": sec_plain, "paper": sec_paper, "ring": sec_ring,
 }
 
 if __name__ == "__main__":

@@ -8,7 +8,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, make_keys
+from conftest import GOLDEN, O, make_keys
 from paper_2309_09025_b200 import bootstrap, errors, lwe, network, neuron, params, rgsw, ring
 
 
@@ -107,7 +107,8 @@ def test_encrypt_decrypt_roundtrip(toy64, toy64_keys):
     assert lwe.decrypt(ct, sk, toy64) == 1
 
 
-def test_gadget_host_rule(desk):
+@pytest.mark.gpu
+def test_gadget_device_rule(desk):
     rng = np.random.default_rng(5)
     x = rng.integers(0, desk.q, (3, 16))
     d = rgsw.gadget_decompose(x, desk.q, desk.gadget)
@@ -221,3 +222,32 @@ def test_paper_model_lowering_known_answers():
         x = (img.astype(np.float64) / 255.0 >= 0.5).astype(np.int64).ravel()
         sc, _, over = O.plain_infer(x, layers, net.T, 2048)
         assert over == 0 and np.array_equal(sc, g[f"plain{k}"])
+
+
+def test_ring_value_types():
+    """ZqElement / NegacyclicPoly / monomial_rotate semantics (ring.py:71-100,
+    146-196, 245-247; reference test_ring.py:58-89)."""
+    from paper_2309_09025_b200 import ring
+    a, b = ring.ZqElement(13, 16), ring.ZqElement(7, 16)
+    assert (a + b).value == 4 and (a - b).value == 6 and (a * b).value == 11 and a.centered == -3
+    with pytest.raises(errors.ParameterError):
+        a + ring.ZqElement(1, 32)
+    N, q = 16, 1 << 10
+    p = ring.NegacyclicPoly(np.arange(N) * 7, q)
+    assert ring.monomial_rotate(p, N) == ring.NegacyclicPoly(-p.coeffs, q)      # half turn negates
+    assert ring.monomial_rotate(p, 2 * N) == p                                   # full turn
+    assert ring.monomial_rotate(ring.monomial_rotate(p, 5), -5) == p
+    assert ring.monomial_rotate(p, 3) == ring.NegacyclicPoly(O.monomial_rotate(p.coeffs, [3], N)[0], q)
+    assert (p + p) - p == p and ring.NegacyclicPoly.zero(N, q) + p == p
+    with pytest.raises(errors.ParameterError):
+        p + ring.NegacyclicPoly.zero(N, 2 * q)
+
+
+def test_reference_architecture_topology():
+    """network.py:214-233: conv 10x8x8/2 (pad 1) -> spike -> pool 2 -> 360->160 -> spike -> 160->10."""
+    from paper_2309_09025_b200 import network
+    m = network.reference_architecture()
+    assert m.shape_chain() == [(10, 12, 12), (10, 12, 12), (10, 6, 6), (160,), (160,), (10,), (10,)]
+    assert [w.shape for w in m.weights] == [(10, 1, 8, 8), (160, 360), (10, 160)]
+    w0 = np.random.default_rng(0).normal(0, 0.1, (10, 1, 8, 8))
+    assert np.array_equal(m.weights[0], w0)

@@ -181,3 +181,31 @@ def test_oracle_plain_infer_golden(tag, desk, c4prm):
             assert np.array_equal(c, g[f"{tag}_counts{li}"][k]), (k, li)
         overflowing += over > 0
     assert overflowing == int(g[f"{tag}_overflow_images"][0])
+
+
+# ---------------------------------------------------- algebra layer (ring.npz)
+
+def test_oracle_transform_matches_reference():
+    """oracle.Transform vs the reference's NegacyclicTransform outputs."""
+    g = load("ring")
+    for N in (2, 8, 64, 1024, 2048):
+        tr = O.Transform(N)
+        f = tr.forward(g[f"nt{N}_in"])
+        scale = np.abs(g[f"nt{N}_fwd"]).max()
+        assert np.abs(f - g[f"nt{N}_fwd"]).max() <= 1e-12 * scale
+        assert np.abs(tr.inverse(g[f"nt{N}_fwd"]) - g[f"nt{N}_inv"]).max() <= 1e-9
+
+
+def test_oracle_products_and_digits_match_reference():
+    g = load("ring")
+    for name in ("desk", "c4", "tiny"):
+        q = int(g[f"mul_{name}_q"][0])
+        assert np.array_equal(O.negacyclic_mul(g[f"mul_{name}_a"], g[f"mul_{name}_b"], q), g[f"mul_{name}_out"])
+    for name in ("desk", "c4", "small"):
+        q, base, levels = (int(v) for v in g[f"dig_{name}_prm"])
+        assert np.array_equal(O.gadget_decompose(g[f"dig_{name}_x"], q, base, levels), g[f"dig_{name}_out"])
+    for name in ("small", "desk"):
+        q, base, levels, _ = (int(v) for v in g[f"ext_{name}_gadget"])
+        ct, rows = g[f"ext_{name}_ct"], g[f"ext_{name}_rows"]
+        oa, ob = O.external_product(ct[0], ct[1], rows[0], rows[1], q, base, levels)
+        assert np.array_equal(np.stack([oa, ob]), g[f"ext_{name}_out"])
