@@ -461,9 +461,11 @@ FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& t
         if constexpr (INV) {
             r2_split(v0, p, tw);
             r2_split(v1, p, tw);
-            fft_stockham2<512, true>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
+            if constexpr (FDSNN_PIPE2) fft_stockham2p<512, true>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
+            else fft_stockham2<512, true>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
         } else {
-            fft_stockham2<512, false>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
+            if constexpr (FDSNN_PIPE2) fft_stockham2p<512, false>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
+            else fft_stockham2<512, false>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
             r2_join(v0, p, tw);
             r2_join(v1, p, tw);
         }
