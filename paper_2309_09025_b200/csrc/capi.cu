@@ -148,10 +148,10 @@ cudaStream_t pick(fdsnn_ctx* ctx, void* stream) {
 }
 
 // V = rotations covered by this launch, starting at a.v_base
-template <int M, int G, bool RAW, bool MARGIN, bool PAIR>
+template <int M, int G, bool RAW, bool MARGIN, bool PAIR, int LQ = 2>
 int launch_br_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_t s) {
     const size_t smem = pbs_smem_bytes<M>(G, 2 * M, ctx->dp.n, PAIR && M == 512 && FDSNN_LY2);
-    auto kern = pbs_blind_rotate_kernel<M, G, RAW, MARGIN, PAIR>;
+    auto kern = pbs_blind_rotate_kernel<M, G, RAW, MARGIN, PAIR, LQ>;
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (V + G - 1) / G;
     kern<<<(unsigned)blocks, G * (M / 8), smem, s>>>(a);
@@ -159,12 +159,12 @@ int launch_br_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_t s) {
     return FDSNN_OK;
 }
 
-template <int M, int G, bool PAIR = false>
+template <int M, int G, bool PAIR = false, int LQ = 2>
 int launch_br_m(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_t s) {
-    if (raw) return ctx->track_margin ? launch_br_t<M, G, true, true, PAIR>(ctx, a, V, s)
-                                      : launch_br_t<M, G, true, false, PAIR>(ctx, a, V, s);
-    return ctx->track_margin ? launch_br_t<M, G, false, true, PAIR>(ctx, a, V, s)
-                             : launch_br_t<M, G, false, false, PAIR>(ctx, a, V, s);
+    if (raw) return ctx->track_margin ? launch_br_t<M, G, true, true, PAIR, LQ>(ctx, a, V, s)
+                                      : launch_br_t<M, G, true, false, PAIR, LQ>(ctx, a, V, s);
+    return ctx->track_margin ? launch_br_t<M, G, false, true, PAIR, LQ>(ctx, a, V, s)
+                             : launch_br_t<M, G, false, false, PAIR, LQ>(ctx, a, V, s);
 }
 
 template <bool RAW, bool MARGIN>
@@ -213,7 +213,13 @@ int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_
             }
             if (V > 2 * 148) return launch_br_m<512, 4>(ctx, a, V, raw, s);
             return launch_br_m<512, 1>(ctx, a, V, raw, s);
-        case 1024: return launch_br_m<1024, 2>(ctx, a, V, raw, s);
+        case 1024: {
+            // C4 (l = 3): the six digit transforms of a step in three
+            // pipelined pairs (FDSNN_C4PAIR=0: one at a time)
+            static const bool pair3 = !(getenv("FDSNN_C4PAIR") && atoi(getenv("FDSNN_C4PAIR")) == 0);
+            if (pair3 && ctx->dp.L == 3) return launch_br_m<1024, 2, true, 3>(ctx, a, V, raw, s);
+            return launch_br_m<1024, 2>(ctx, a, V, raw, s);
+        }
     }
     return set_err(FDSNN_ERR_PARAMETER, "unsupported ring degree N=%d", ctx->dp.N);
 }

@@ -164,7 +164,7 @@ constexpr uint32_t PBS_TMEM_OWN = 128;
 // pair per exchange) and MAC'd together; the first polynomial's partial
 // frequency accumulators wait in TMEM (columns 256 + 64*(w/4)) while the
 // second polynomial is transformed.
-template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN, bool PAIR = false>
+template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN, bool PAIR = false, int LQ = 2>
 __global__ void __launch_bounds__(G * (M / 8), 1)
 pbs_blind_rotate_kernel(const PbsArgs args) {
     constexpr uint32_t TMEM_COLS = PAIR ? 512 : PBS_TMEM_COLS;
@@ -373,20 +373,29 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     }
                 }
             }
-#pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-                int32_t xlo[8], xhi[8];
+            // y = centred((X^k - 1) ACC) + H of poly cc, lo/hi halves
+            auto make_x = [&](int cc, int32_t (&xlo)[8], int32_t (&xhi)[8]) {
                 uint32_t ow[16];
                 tmem_ld16_async(own_col + 16 * cc, ow);
                 const uint32_t (&rv)[16] = rvs[cc];
                 tmem_wait16(ow);
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
-                    // y = centred((X^k - 1) ACC) + H
                     xlo[r] = (int32_t)((rv[r] - ow[r] + halfq) & qmask) + yoff;
                     xhi[r] = (int32_t)((rv[8 + r] - ow[8 + r] + halfq) & qmask) + yoff;
                 }
-                if constexpr (PAIR) {
+            };
+            if constexpr (PAIR) {
+                // The 2*LQ digit polynomials (poly cc, level lvl) in key-chunk
+                // order f = cc*LQ + lvl, transformed two at a time; the
+                // frequency sums of all but the last pair are parked in TMEM.
+                int32_t xlo[2][8], xhi[2][8];
+                make_x(0, xlo[0], xhi[0]);
+#pragma unroll
+                for (int pr = 0; pr < LQ; ++pr) {
+                    const int fa = 2 * pr, fb = 2 * pr + 1;
+                    const int ca = fa / LQ, la = fa % LQ, cb = fb / LQ, lb = fb % LQ;
+                    if (pr == LQ / 2) make_x(1, xlo[1], xhi[1]);  // first pair touching poly 1
                     double2 v0[8], v1[8];
                     {
                         uint32_t twr[32];
@@ -394,10 +403,10 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                         int32_t d1[8], d2[8], e1[8], e2[8];
 #pragma unroll
                         for (int r = 0; r < 8; ++r) {
-                            d1[r] = (xlo[r] & bmask) - halfB1;
-                            d2[r] = (xhi[r] & bmask) - halfB1;
-                            e1[r] = ((xlo[r] >> bg) & bmask) - halfB1;
-                            e2[r] = ((xhi[r] >> bg) & bmask) - halfB1;
+                            d1[r] = ((xlo[ca][r] >> (bg * la)) & bmask) - halfB1;
+                            d2[r] = ((xhi[ca][r] >> (bg * la)) & bmask) - halfB1;
+                            e1[r] = ((xlo[cb][r] >> (bg * lb)) & bmask) - halfB1;
+                            e2[r] = ((xhi[cb][r] >> (bg * lb)) & bmask) - halfB1;
                         }
                         tmem_wait32(twr);
 #pragma unroll
@@ -425,13 +434,24 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     }
                     const double2* k0 = ring + (size_t)s0 * 2 * M;
                     const double2* k1 = ring + (size_t)s1 * 2 * M;
-                    if (cc == 0) {
+                    if (pr < LQ - 1) {  // partial sums -> TMEM
+                        if (pr > 0) {
+                            uint32_t oa[32], ob[32];
+                            tmem_ld32_async(o_col, oa);
+                            tmem_ld32_async(o_col + 32, ob);
+                            tmem_wait64(oa, ob);
+#pragma unroll
+                            for (int r = 0; r < 8; ++r) {
+                                O0[r] = words_c(oa, r);
+                                O1[r] = words_c(ob, r);
+                            }
+                        }
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             uint32_t ow2[32];
 #pragma unroll
                             for (int r = 0; r < 8; ++r) {
-                                double2 o = make_double2(0.0, 0.0);
+                                double2 o = pr > 0 ? (h ? O1[r] : O0[r]) : make_double2(0.0, 0.0);
                                 cmac(o, v0[r], k0[h * M + t + r * T]);
                                 cmac(o, v1[r], k1[h * M + t + r * T]);
                                 put_words_c(ow2, r, o);
@@ -457,7 +477,12 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     release(c);
                     release(c + 1);
                     c += 2;
-                } else
+                }
+            } else {
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                int32_t xlo[8], xhi[8];
+                make_x(cc, xlo, xhi);
                 for (int lvl = 0; lvl < L; ++lvl, ++c) {
                     double2 vv[8];
                     {
@@ -487,6 +512,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     }
                     release(c);
                 }
+            }
             }
             {
                 uint32_t twr[32], own[32];
