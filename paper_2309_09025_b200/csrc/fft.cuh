@@ -303,7 +303,7 @@ FDSNN_DEV void fft_stockham2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW
 // hide the load latency) instead of by its own consumer.  Each barrier is the
 // read-after-write fence of one buffer and the write-after-read fence of the
 // other: 2P-1 barriers per pair against 2(P-1) for fft_stockham2.
-template <int M, bool INV, class TW, class HOOK = NoHook>
+template <int M, bool INV, class TW, class HOOK = NoHook, bool ENTRY_SYNC = true>
 FDSNN_DEV void fft_stockham2p(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& tw,
                               double2* __restrict__ buf0, double2* __restrict__ buf1,
                               const GroupSync& gs, const HOOK& pre_last = HOOK()) {
@@ -312,7 +312,7 @@ FDSNN_DEV void fft_stockham2p(double2 (&v0)[8], double2 (&v1)[8], int t, const T
     {
         double2 w[8];
         pass_body<M, 0, INV>(v0, w);
-        gs.sync();  // previous readers of both buffers are done
+        if constexpr (ENTRY_SYNC) gs.sync();  // previous readers of both buffers are done
         pass_store<M, 0>(v0, t, buf0);
         gs.sync();
         pass_load<M, 1>(v0, t, buf0);
@@ -450,7 +450,7 @@ FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
     }
 }
 
-template <int M, bool INV, class TW, class HOOK = NoHook>
+template <int M, bool INV, class TW, class HOOK = NoHook, bool ENTRY_SYNC = true>
 FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& tw,
                           double2* __restrict__ buf0, double2* __restrict__ buf1,
                           const GroupSync& gs, const HOOK& pre_last = HOOK()) {
@@ -461,16 +461,16 @@ FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& t
         if constexpr (INV) {
             r2_split(v0, p, tw);
             r2_split(v1, p, tw);
-            if constexpr (FDSNN_PIPE2) fft_stockham2p<512, true>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
+            if constexpr (FDSNN_PIPE2) fft_stockham2p<512, true, decltype(tw.sub()), HOOK, ENTRY_SYNC>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
             else fft_stockham2<512, true>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
         } else {
-            if constexpr (FDSNN_PIPE2) fft_stockham2p<512, false>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
+            if constexpr (FDSNN_PIPE2) fft_stockham2p<512, false, decltype(tw.sub()), HOOK, ENTRY_SYNC>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
             else fft_stockham2<512, false>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
             r2_join(v0, p, tw);
             r2_join(v1, p, tw);
         }
     } else if constexpr (FDSNN_PIPE2 && Schedule<M>::P == 3) {
-        fft_stockham2p<M, INV>(v0, v1, t, tw, buf0, buf1, gs, pre_last);
+        fft_stockham2p<M, INV, TW, HOOK, ENTRY_SYNC>(v0, v1, t, tw, buf0, buf1, gs, pre_last);
     } else {
         fft_stockham2<M, INV>(v0, v1, t, tw, buf0, buf1, gs, pre_last);
     }

@@ -32,6 +32,9 @@
 #pragma once
 #include "fft.cuh"
 #include "fft2.cuh"
+#ifndef FDSNN_SKIP_ENTRY
+#define FDSNN_SKIP_ENTRY 1
+#endif
 #ifndef FDSNN_EARLY_KEYS
 #define FDSNN_EARLY_KEYS 1
 #endif
@@ -427,7 +430,13 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                         fft2_fwd_pair(v0, v1, t, tw2, xbuf, buf0, buf1, x_col, gs);
                         keys_ready();
                     } else if constexpr (FDSNN_EARLY_KEYS) {
-                        fft_group2<M, false>(v0, v1, t, tw, buf0, buf1, gs, keys_ready);
+                        // the first pair of a step follows the step's closing
+                        // barrier, which already fences the buffers' last readers
+                        if (pr == 0 && FDSNN_SKIP_ENTRY)
+                            fft_group2<M, false, TwiddlesInTmem<M>, decltype(keys_ready), false>(
+                                v0, v1, t, tw, buf0, buf1, gs, keys_ready);
+                        else
+                            fft_group2<M, false>(v0, v1, t, tw, buf0, buf1, gs, keys_ready);
                     } else {
                         fft_group2<M, false>(v0, v1, t, tw, buf0, buf1, gs);
                         keys_ready();
