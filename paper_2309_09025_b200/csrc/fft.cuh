@@ -48,14 +48,12 @@ FDSNN_DEV void dft4(double2& y0, double2& y1, double2& y2, double2& y3) {
     y3 = csub(c1, c3);
 }
 
-// 8-point DFT with kernel e^{s 2 pi i/8}, natural order in/out.
+// Second half of the 8-point DFT from the first-stage sums a_r = x_r + x_{r+4}
+// and differences b_r = x_r - x_{r+4}.
 template <bool INV>
-FDSNN_DEV void dft8(double2* v) {
+FDSNN_DEV void dft8_tail(double2* v, double2 a0, double2 a1, double2 a2, double2 a3,
+                         double2 b0, double2 b1, double2 b2, double2 b3) {
     const double h = 0.70710678118654752440;  // sqrt(2)/2
-    double2 a0 = cadd(v[0], v[4]), b0 = csub(v[0], v[4]);
-    double2 a1 = cadd(v[1], v[5]), b1 = csub(v[1], v[5]);
-    double2 a2 = cadd(v[2], v[6]), b2 = csub(v[2], v[6]);
-    double2 a3 = cadd(v[3], v[7]), b3 = csub(v[3], v[7]);
     // odd outputs = DFT4(b0, b1 e^{s i pi/4}, b2 (s i), b3 e^{s 3i pi/4}).  The
     // sqrt(2)/2 of the two diagonal twiddles is folded into the final FMAs:
     // u1 = (1 + s i) b1, u3 = (-1 + s i) b3 cost additions only.
@@ -73,6 +71,49 @@ FDSNN_DEV void dft8(double2* v) {
     v[5] = make_double2(fma(-h, e.x, c0.x), fma(-h, e.y, c0.y));
     v[3] = make_double2(fma(h, f.x, c1.x), fma(h, f.y, c1.y));
     v[7] = make_double2(fma(-h, f.x, c1.x), fma(-h, f.y, c1.y));
+}
+
+// 8-point DFT with kernel e^{s 2 pi i/8}, natural order in/out.
+template <bool INV>
+FDSNN_DEV void dft8(double2* v) {
+    dft8_tail<INV>(v, cadd(v[0], v[4]), cadd(v[1], v[5]), cadd(v[2], v[6]), cadd(v[3], v[7]),
+                   csub(v[0], v[4]), csub(v[1], v[5]), csub(v[2], v[6]), csub(v[3], v[7]));
+}
+
+#ifndef FDSNN_FUSED_TW
+#define FDSNN_FUSED_TW 1
+#endif
+// c + w v  (CONJ: c + conj(w) v), four DFMA
+template <bool CONJ>
+FDSNN_DEV double2 cfma(double2 c, double2 w, double2 v) {
+    if constexpr (CONJ)
+        return make_double2(fma(w.y, v.y, fma(w.x, v.x, c.x)), fma(-w.y, v.x, fma(w.x, v.y, c.y)));
+    else
+        return make_double2(fma(-w.y, v.y, fma(w.x, v.x, c.x)), fma(w.y, v.x, fma(w.x, v.y, c.y)));
+}
+// 2t - a, two DFMA
+FDSNN_DEV double2 ctwo_minus(double2 t, double2 a) {
+    return make_double2(fma(2.0, t.x, -a.x), fma(2.0, t.y, -a.y));
+}
+
+// 8-point DFT of the input-twiddled points x_r = w_r v_r with the twiddle
+// products fused into the first butterfly stage:  a_r = t_r + w_{r+4} v_{r+4}
+// (t_r = w_r v_r; four DFMA) and b_r = 2 t_r - a_r (two DFMA) instead of two
+// complex products and two complex additions -- 8 fewer FP64 instructions
+// per radix-8 pass.  W0 = false: v_0 is not twiddled (interior passes,
+// w[r-1] = w_r); W0 = true: all eight are (the forward twist, w[r] = w_r).
+template <bool INV, bool W0>
+FDSNN_DEV void dft8_tw(double2* v, const double2* w) {
+    auto wr = [&](int r) { return W0 ? w[r] : w[r - 1]; };
+    auto tr = [&](int r) {
+        if (r == 0 && !W0) return v[0];
+        return INV ? cmulc(v[r], wr(r)) : cmul(v[r], wr(r));
+    };
+    const double2 t0 = tr(0), t1 = tr(1), t2 = tr(2), t3 = tr(3);
+    const double2 a0 = cfma<INV>(t0, wr(4), v[4]), a1 = cfma<INV>(t1, wr(5), v[5]);
+    const double2 a2 = cfma<INV>(t2, wr(6), v[6]), a3 = cfma<INV>(t3, wr(7), v[7]);
+    dft8_tail<INV>(v, a0, a1, a2, a3, ctwo_minus(t0, a0), ctwo_minus(t1, a1), ctwo_minus(t2, a2),
+                   ctwo_minus(t3, a3));
 }
 
 template <int R, bool INV>
@@ -186,6 +227,10 @@ template <int M, int PASS, bool INV>
 FDSNN_DEV void pass_body(double2 (&v)[8], const double2 (&w)[8]) {
     constexpr int R = PassInfo<M, PASS>::R;
     constexpr int NS = PassInfo<M, PASS>::NS;
+    if constexpr (FDSNN_FUSED_TW && R == 8 && NS > 1) {
+        dft8_tw<INV, false>(v, w);
+        return;
+    }
 #pragma unroll
     for (int s = 0; s < 8 / R; ++s) {
         if constexpr (NS > 1) {
@@ -303,20 +348,33 @@ FDSNN_DEV void fft_stockham2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW
 // hide the load latency) instead of by its own consumer.  Each barrier is the
 // read-after-write fence of one buffer and the write-after-read fence of the
 // other: 2P-1 barriers per pair against 2(P-1) for fft_stockham2.
-template <int M, bool INV, class TW, class HOOK = NoHook, bool ENTRY_SYNC = true>
+// FT0: the inputs still need the per-point factors tw0[r] (the forward
+// twist); they are fused into the first pass (dft8_tw).
+template <int M, bool INV, bool FT0>
+FDSNN_DEV void first_pass(double2 (&v)[8], const double2* tw0) {
+    if constexpr (FT0) {
+        dft8_tw<INV, true>(v, tw0);
+    } else {
+        double2 w[8];
+        pass_body<M, 0, INV>(v, w);
+    }
+}
+
+template <int M, bool INV, class TW, class HOOK = NoHook, bool ENTRY_SYNC = true, bool FT0 = false>
 FDSNN_DEV void fft_stockham2p(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& tw,
                               double2* __restrict__ buf0, double2* __restrict__ buf1,
-                              const GroupSync& gs, const HOOK& pre_last = HOOK()) {
+                              const GroupSync& gs, const HOOK& pre_last = HOOK(),
+                              const double2* tw0 = nullptr) {
     constexpr int P = Schedule<M>::P;
     static_assert(P == 3, "pipelined pair written for three passes");
+    static_assert(!FT0 || Schedule<M>::R[0] == 8, "fused twist needs a radix-8 first pass");
     {
-        double2 w[8];
-        pass_body<M, 0, INV>(v0, w);
+        first_pass<M, INV, FT0>(v0, tw0);
         if constexpr (ENTRY_SYNC) gs.sync();  // previous readers of both buffers are done
         pass_store<M, 0>(v0, t, buf0);
         gs.sync();
         pass_load<M, 1>(v0, t, buf0);
-        pass_body<M, 0, INV>(v1, w);
+        first_pass<M, INV, FT0>(v1, tw0);
     }
     {
         uint32_t raw[32];
@@ -450,10 +508,12 @@ FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
     }
 }
 
-template <int M, bool INV, class TW, class HOOK = NoHook, bool ENTRY_SYNC = true>
+template <int M, bool INV, class TW, class HOOK = NoHook, bool ENTRY_SYNC = true, bool FT0 = false>
 FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& tw,
                           double2* __restrict__ buf0, double2* __restrict__ buf1,
-                          const GroupSync& gs, const HOOK& pre_last = HOOK()) {
+                          const GroupSync& gs, const HOOK& pre_last = HOOK(),
+                          const double2* tw0 = nullptr) {
+    static_assert(!FT0 || (FDSNN_PIPE2 && !INV), "fused twist: pipelined forward pairs only");
     if constexpr (M == 1024) {
         const int p = t & 1;
         double2* b0 = buf0 + p * FFT1024_HALF;
@@ -464,13 +524,13 @@ FDSNN_DEV void fft_group2(double2 (&v0)[8], double2 (&v1)[8], int t, const TW& t
             if constexpr (FDSNN_PIPE2) fft_stockham2p<512, true, decltype(tw.sub()), HOOK, ENTRY_SYNC>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
             else fft_stockham2<512, true>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
         } else {
-            if constexpr (FDSNN_PIPE2) fft_stockham2p<512, false, decltype(tw.sub()), HOOK, ENTRY_SYNC>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
+            if constexpr (FDSNN_PIPE2) fft_stockham2p<512, false, decltype(tw.sub()), HOOK, ENTRY_SYNC, FT0>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last, tw0);
             else fft_stockham2<512, false>(v0, v1, t >> 1, tw.sub(), b0, b1, gs, pre_last);
             r2_join(v0, p, tw);
             r2_join(v1, p, tw);
         }
     } else if constexpr (FDSNN_PIPE2 && Schedule<M>::P == 3) {
-        fft_stockham2p<M, INV, TW, HOOK, ENTRY_SYNC>(v0, v1, t, tw, buf0, buf1, gs, pre_last);
+        fft_stockham2p<M, INV, TW, HOOK, ENTRY_SYNC, FT0>(v0, v1, t, tw, buf0, buf1, gs, pre_last, tw0);
     } else {
         fft_stockham2<M, INV>(v0, v1, t, tw, buf0, buf1, gs, pre_last);
     }

@@ -38,6 +38,9 @@
 #ifndef FDSNN_EARLY_KEYS
 #define FDSNN_EARLY_KEYS 1
 #endif
+#ifndef FDSNN_SKEW
+#define FDSNN_SKEW 0  // start half the accumulators of a CTA late: 1 = one transform pair, 2 = ~0.6 pair
+#endif
 #ifndef FDSNN_LY2
 #define FDSNN_LY2 0  // layout-2 transforms (fft2.cuh): bit-exact, 2.5% slower on B200 (DESIGN 8)
 #endif
@@ -209,7 +212,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     const int64_t v0 = args.v_base + (int64_t)blockIdx.x * G;
     const int nact = (int)((V - v0) < G ? (V - v0) : G);  // active groups in this CTA
     const bool active = g < nact;
-    const int64_t nchunks = (int64_t)n * 2 * L;
+    const int nchunks = n * 2 * L;  // 32-bit: stage index and phase by constant division
     const bool producer = threadIdx.x == 0;
     if (producer) {
         for (int s = 0; s < S; ++s) {
@@ -268,10 +271,15 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
             bulk_g2s(ring + (size_t)s * 2 * M, args.bsk + (size_t)s * 2 * M, CHUNK, &full[s]);
         }
     }
-    auto release = [&](int64_t c) {
+    // With the phase skew the refills are issued by the last (trailing) group:
+    // by the time it releases a stage every leading group has released it too,
+    // so the refill never waits on a group that is half a step behind.
+    const bool skewed = PAIR && FDSNN_SKEW && G == 4 && nact > G / 2;
+    const bool refiller = threadIdx.x == (skewed ? (nact - 1) * T : 0);
+    auto release = [&](int c) {
         const int s = (int)(c % S);
         mbar_arrive(&empty[s]);
-        if (producer && c + S < nchunks) {
+        if (refiller && c + S < nchunks) {
             mbar_wait(&empty[s], (uint32_t)((c / S) & 1));
             mbar_arrive_expect_tx(&full[s], CHUNK);
             bulk_g2s(ring + (size_t)s * 2 * M, args.bsk + (size_t)(c + S) * 2 * M, CHUNK, &full[s]);
@@ -342,7 +350,17 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
         int ex = 0;
         double err_max = 0.0;
 
-        int64_t c = 0;  // chunk counter = i * 2L + digit
+        // Phase skew: the leading half of the accumulators signals after the
+        // first pair of step 0 and the trailing half starts only then, so the
+        // two warps of a scheduler (groups g and g + G/2) stay half a step
+        // apart -- one in its exchanges while the other runs butterflies.
+        const bool lead = g < G / 2;
+        auto skew_arrive = [&]() {
+            if (skewed && lead) asm volatile("bar.arrive 15, %0;" ::"r"(T * nact) : "memory");
+        };
+        if (skewed && !lead) named_bar(15, T * nact);
+
+        int c = 0;      // chunk counter = i * 2L + digit
         for (int i = 0; i < n; ++i) {
             const int k = a2N[i];
             if (k == 0) {  // X^0*ACC - ACC = 0: identity step; keep the key pipeline in sync
@@ -350,6 +368,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     mbar_wait(&full[c % S], (uint32_t)((c / S) & 1));
                     release(c);
                 }
+                if (i == 0) skew_arrive();
                 continue;
             }
             double2 O0[8], O1[8];
@@ -400,6 +419,8 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     const int ca = fa / LQ, la = fa % LQ, cb = fb / LQ, lb = fb % LQ;
                     if (pr == LQ / 2) make_x(1, xlo[1], xhi[1]);  // first pair touching poly 1
                     double2 v0[8], v1[8];
+                    constexpr bool FT = FDSNN_FUSED_TW && !LY2;
+                    double2 twv[8];
                     {
                         uint32_t twr[32];
                         tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
@@ -415,14 +436,21 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
 #pragma unroll
                         for (int r = 0; r < 8; ++r) {
                             const double2 tr = words_c(twr, r);
-                            v0[r] = cmul(make_double2((double)d1[r], (double)d2[r]), tr);
-                            v1[r] = cmul(make_double2((double)e1[r], (double)e2[r]), tr);
+                            if constexpr (FT) {  // twist fused into the first pass
+                                twv[r] = tr;
+                                v0[r] = make_double2((double)d1[r], (double)d2[r]);
+                                v1[r] = make_double2((double)e1[r], (double)e2[r]);
+                            } else {
+                                v0[r] = cmul(make_double2((double)d1[r], (double)d2[r]), tr);
+                                v1[r] = cmul(make_double2((double)e1[r], (double)e2[r]), tr);
+                            }
                         }
                     }
                     const int s0 = (int)(c % S), s1 = (int)((c + 1) % S);
                     // key chunks landed: waited for before the last pass, so
                     // the MAC's key loads may be scheduled into it
                     auto keys_ready = [&]() {
+                        if (FDSNN_SKEW == 2 && i == 0 && pr == 0) skew_arrive();
                         mbar_wait(&full[s0], (uint32_t)((c / S) & 1));
                         mbar_wait(&full[s1], (uint32_t)(((c + 1) / S) & 1));
                     };
@@ -433,10 +461,11 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                         // the first pair of a step follows the step's closing
                         // barrier, which already fences the buffers' last readers
                         if (pr == 0 && FDSNN_SKIP_ENTRY)
-                            fft_group2<M, false, TwiddlesInTmem<M>, decltype(keys_ready), false>(
-                                v0, v1, t, tw, buf0, buf1, gs, keys_ready);
+                            fft_group2<M, false, TwiddlesInTmem<M>, decltype(keys_ready), false, FT>(
+                                v0, v1, t, tw, buf0, buf1, gs, keys_ready, twv);
                         else
-                            fft_group2<M, false>(v0, v1, t, tw, buf0, buf1, gs, keys_ready);
+                            fft_group2<M, false, TwiddlesInTmem<M>, decltype(keys_ready), true, FT>(
+                                v0, v1, t, tw, buf0, buf1, gs, keys_ready, twv);
                     } else {
                         fft_group2<M, false>(v0, v1, t, tw, buf0, buf1, gs);
                         keys_ready();
@@ -486,6 +515,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     release(c);
                     release(c + 1);
                     c += 2;
+                    if (FDSNN_SKEW == 1 && i == 0 && pr == 0) skew_arrive();
                 }
             } else {
 #pragma unroll
@@ -539,18 +569,23 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     const double2 tr = words_c(twr, r);
                     const double2 z0 = cmulc(O0[r], tr);
                     const double2 z1 = cmulc(O1[r], tr);
-                    const long long r00 = round_product(z0.x), r01 = round_product(z0.y);
-                    const long long r10 = round_product(z1.x), r11 = round_product(z1.y);
+                    uint32_t r00, r01, r10, r11;
                     if constexpr (TRACK_MARGIN) {
-                        err_max = fmax(err_max, fabs(z0.x - (double)r00));
-                        err_max = fmax(err_max, fabs(z0.y - (double)r01));
-                        err_max = fmax(err_max, fabs(z1.x - (double)r10));
-                        err_max = fmax(err_max, fabs(z1.y - (double)r11));
+                        const long long e00 = round_product(z0.x), e01 = round_product(z0.y);
+                        const long long e10 = round_product(z1.x), e11 = round_product(z1.y);
+                        err_max = fmax(err_max, fabs(z0.x - (double)e00));
+                        err_max = fmax(err_max, fabs(z0.y - (double)e01));
+                        err_max = fmax(err_max, fabs(z1.x - (double)e10));
+                        err_max = fmax(err_max, fabs(z1.y - (double)e11));
+                        r00 = (uint32_t)e00; r01 = (uint32_t)e01; r10 = (uint32_t)e10; r11 = (uint32_t)e11;
+                    } else {
+                        r00 = round_lo32(z0.x); r01 = round_lo32(z0.y);
+                        r10 = round_lo32(z1.x); r11 = round_lo32(z1.y);
                     }
-                    own[r] = (own[r] + (uint32_t)r00) & qmask;
-                    own[8 + r] = (own[8 + r] + (uint32_t)r01) & qmask;
-                    own[16 + r] = (own[16 + r] + (uint32_t)r10) & qmask;
-                    own[24 + r] = (own[24 + r] + (uint32_t)r11) & qmask;
+                    own[r] = (own[r] + r00) & qmask;
+                    own[8 + r] = (own[8 + r] + r01) & qmask;
+                    own[16 + r] = (own[16 + r] + r10) & qmask;
+                    own[24 + r] = (own[24 + r] + r11) & qmask;
                     acc[p] = (int32_t)own[r];
                     acc[pM] = (int32_t)own[8 + r];
                     acc[NA + p] = (int32_t)own[16 + r];
@@ -680,10 +715,12 @@ pbs_blind_rotate_wide_kernel(const PbsArgs args) {
         }
     }
     // stage s always holds digit s of the current step; warp-pair s releases
-    // it after its MAC, and after the step's CTA barrier the producer loads
-    // the next step's chunks into all stages
+    // it after its MAC, and after the step's CTA barrier the last warp-pair
+    // (idle while pairs 0 and 1 run the inverse transforms, so the copies are
+    // issued off the critical path) loads the next step's chunks
+    const bool refiller = threadIdx.x == (L2 - 1) * T;
     auto refill = [&](int i) {
-        if (producer && (int64_t)(i + 1) * L2 < nchunks) {
+        if (refiller && (int64_t)(i + 1) * L2 < nchunks) {
             for (int s = 0; s < S; ++s) {
                 mbar_wait(&empty[s], (uint32_t)(i & 1));
                 mbar_arrive_expect_tx(&full[s], CHUNK);
