@@ -39,7 +39,7 @@
 #define FDSNN_EARLY_KEYS 1
 #endif
 #ifndef FDSNN_SKEW
-#define FDSNN_SKEW 0  // start half the accumulators of a CTA late: 1 = one transform pair, 2 = ~0.6 pair
+#define FDSNN_SKEW 1  // start half the accumulators of a CTA late: 1 = one transform pair, 2 = ~0.6 pair
 #endif
 #ifndef FDSNN_LY2
 #define FDSNN_LY2 0  // layout-2 transforms (fft2.cuh): bit-exact, 2.5% slower on B200 (DESIGN 8)
@@ -88,7 +88,7 @@ __host__ __device__ constexpr size_t pbs_group_bytes(int N, int n, bool ly2 = fa
 
 constexpr int PBS_THREADS = 256;
 #ifndef FDSNN_RING_S
-#define FDSNN_RING_S 4
+#define FDSNN_RING_S 5
 #endif
 template <int M> struct PbsRing { static constexpr int S = (M == 1024) ? 3 : FDSNN_RING_S; };
 static_assert(FDSNN_RING_S >= 2 && FDSNN_RING_S <= 7, "mbarriers live in the 120-byte ring header");
