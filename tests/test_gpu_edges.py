@@ -123,11 +123,14 @@ def test_fdsn_containers_to_device(toy, toy_keys, tmp_path):
         serial.load_bootstrap_key_device(tmp_path / "ct.bin", toy)
 
 
-@pytest.mark.parametrize("count", [148, 149, 296, 297, 445, 600, 740, 1040])
+@pytest.mark.parametrize("count", [148, 149, 296, 297, 445, 446, 447, 600, 740, 1040])
 def test_launch_regime_boundaries(desk, desk_keys, count):
     """Batches either side of the launch-split points (full rounds of 4
     rotations per SM, remainder on the latency kernel or at 2-3 per SM) give
-    oracle-identical outputs (first and last 6 checked)."""
+    oracle-identical outputs (first and last 6 checked).  445-447 end the
+    4-rotation launch with a CTA of 1, 2 and 3 active rotations: 3 is the
+    phase-skewed case with a single trailing group (which also refills the
+    key ring), 1-2 run unskewed."""
     sk, _, bsk = desk_keys
     rng = np.random.default_rng(count)
     A, b = lwe.encrypt_batch(rng.integers(-511, 513, count), sk, desk, rng)
