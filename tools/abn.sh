@@ -16,7 +16,7 @@ wait
 NV=$i
 for ((v=1; v<NV; v++)); do
   cp /tmp/V$v.so $L/libfdsnn_b200.so
-  echo "== tests V$v: $(timeout 240 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py -x -q 2>&1 | tail -1)"
+  echo "== tests V$v: $(timeout 300 python -m pytest ${TESTS:-tests/test_gpu_parity.py tests/test_gpu_golden.py} -x -q 2>&1 | tail -1)"
 done
 for rep in 1 2; do
   for ((v=0; v<NV; v++)); do
