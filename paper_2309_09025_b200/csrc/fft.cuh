@@ -278,12 +278,16 @@ struct NoHook {
 // `pre_last` runs after the last exchange and twiddle fetch, before the last
 // pass's arithmetic
 // (used to start the key fetch of the following MAC).
-template <int M, bool INV, class TW, class HOOK = NoHook>
+template <int M, bool INV, class TW, class HOOK = NoHook, bool FT0 = false>
 FDSNN_DEV void fft_stockham(double2 (&v)[8], int t, const TW& tw,
                             double2* __restrict__ buf0, double2* __restrict__ buf1,
-                            int& ex, const GroupSync& gs, const HOOK& pre_last = HOOK()) {
+                            int& ex, const GroupSync& gs, const HOOK& pre_last = HOOK(),
+                            const double2* tw0 = nullptr) {
     constexpr int P = Schedule<M>::P;
-    {
+    static_assert(!FT0 || Schedule<M>::R[0] == 8, "fused twist needs a radix-8 first pass");
+    if constexpr (FT0) {
+        dft8_tw<INV, true>(v, tw0);
+    } else {
         double2 w[8];
         pass_body<M, 0, INV>(v, w);
     }
@@ -488,10 +492,12 @@ FDSNN_DEV void r2_split(double2 (&v)[8], int p, const TW& tw) {
         v[r] = cmulc(make_double2(fma(s, v[r].x, o[r].x), fma(s, v[r].y, o[r].y)), w[r]);
 }
 
-template <int M, bool INV, class TW, class HOOK = NoHook>
+template <int M, bool INV, class TW, class HOOK = NoHook, bool FT0 = false>
 FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
                          double2* __restrict__ buf0, double2* __restrict__ buf1,
-                         int& ex, const GroupSync& gs, const HOOK& pre_last = HOOK()) {
+                         int& ex, const GroupSync& gs, const HOOK& pre_last = HOOK(),
+                         const double2* tw0 = nullptr) {
+    static_assert(!FT0 || (M != 1024 && !INV), "fused twist: M <= 512 forward only");
     if constexpr (M == 1024) {
         const int p = t & 1;
         double2* b0 = buf0 + p * FFT1024_HALF;
@@ -504,7 +510,7 @@ FDSNN_DEV void fft_group(double2 (&v)[8], int t, const TW& tw,
             r2_join(v, p, tw);
         }
     } else {
-        fft_stockham<M, INV>(v, t, tw, buf0, buf1, ex, gs, pre_last);
+        fft_stockham<M, INV, TW, HOOK, FT0>(v, t, tw, buf0, buf1, ex, gs, pre_last, tw0);
     }
 }
 

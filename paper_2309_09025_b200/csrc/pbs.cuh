@@ -782,7 +782,7 @@ pbs_blind_rotate_wide_kernel(const PbsArgs args) {
             continue;
         }
         // digit `lvl` of poly `cc` of (X^k - 1) * ACC
-        double2 vv[8];
+        double2 vv[8], twv[8];
         {
             const int32_t* a = acc + cc * N;
             uint32_t twr[32];
@@ -801,18 +801,30 @@ pbs_blind_rotate_wide_kernel(const PbsArgs args) {
             }
             tmem_wait32(twr);
 #pragma unroll
-            for (int r = 0; r < 8; ++r)
-                vv[r] = cmul(make_double2((double)d1[r], (double)d2[r]), words_c(twr, r));
+            for (int r = 0; r < 8; ++r) {  // the twist is fused into the first pass
+                twv[r] = words_c(twr, r);
+                vv[r] = make_double2((double)d1[r], (double)d2[r]);
+            }
         }
-        fft_group<M, false>(vv, t, tw, buf0, buf1, ex, gs);
-        mbar_wait(&full[wp], (uint32_t)(i & 1));
+        // the key chunk is waited for and read into registers before the
+        // transform's last pass, so those loads overlap its butterflies
         const double2* kd = ring + (size_t)wp * 2 * M;
+        double2 k0[8], k1[8];
+        auto fetch_key = [&]() {
+            mbar_wait(&full[wp], (uint32_t)(i & 1));
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                k0[r] = kd[t + r * T];
+                k1[r] = kd[M + t + r * T];
+            }
+        };
+        fft_group<M, false, TwiddlesInTmem<M>, decltype(fetch_key), true>(vv, t, tw, buf0, buf1, ex, gs, fetch_key, twv);
         gs.sync();  // the transform's last exchange reads are done before the partials overwrite
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             double2 o0 = make_double2(0.0, 0.0), o1 = make_double2(0.0, 0.0);
-            cmac(o0, vv[r], kd[t + r * T]);
-            cmac(o1, vv[r], kd[M + t + r * T]);
+            cmac(o0, vv[r], k0[r]);
+            cmac(o1, vv[r], k1[r]);
             buf0[t + r * T] = o0;  // partial sums of output poly 0
             buf1[t + r * T] = o1;  // and 1
         }
