@@ -178,16 +178,20 @@ def test_n1024_three_level_gadget_paths():
             assert np.array_equal(oA[sl], wA) and np.array_equal(ob[sl], wb), count
 
 
-@pytest.mark.parametrize("count", [5, 400])
+@pytest.mark.parametrize("count", [5, 400, 599])
 def test_desk_blind_rotate_raw_mode(desk, desk_keys, count):
-    """blind_rotate_batch at DESK through the latency kernel (5) and the paired
-    kernel (400), raw accumulators in and out, vs the oracle (3 checked)."""
+    """blind_rotate_batch at DESK through the latency kernel (5), the paired
+    kernel at 3 rotations per CTA (400) and the phase-skewed 4-rotation kernel
+    plus a latency-kernel tail (599), raw accumulators in and out, vs the
+    oracle.  Every third rotation starts with an identity step (rotation 0),
+    the skew's signalling path when it falls on a leading accumulator."""
     sk, _, bsk = desk_keys
     rng = np.random.default_rng(40 + count)
     acc = rng.integers(0, desk.q, (count, 2, desk.N))
     a2N = rng.integers(0, 2 * desk.N, (count, desk.n))
+    a2N[::3, 0] = 0
     got = bootstrap.blind_rotate_batch(acc, a2N, bsk)
     key = oracle_key(desk, bsk)
-    for j in (0, count // 2, count - 1):
+    for j in sorted({0, 1, 3, count // 2, count - 1}):
         want = O.blind_rotate(acc[j:j + 1], a2N[j:j + 1], key)
         assert np.array_equal(got[j:j + 1], want), j
