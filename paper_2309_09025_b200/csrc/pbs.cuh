@@ -87,6 +87,16 @@ __host__ __device__ constexpr size_t pbs_group_bytes(int N, int n, bool ly2 = fa
 }
 
 constexpr int PBS_THREADS = 256;
+// Groups are PBS_GROUP_PAD bytes apart beyond their size (a multiple of 128 B),
+// so two interleaved groups' 16-byte exchange accesses fall in opposite halves
+// of the 32 banks.
+constexpr size_t PBS_GROUP_PAD = 64;
+#ifndef FDSNN_ILV
+#define FDSNN_ILV 1  // M = 512, G = 4: accumulator pairs interleaved lane by lane (key loads broadcast)
+#endif
+#ifndef FDSNN_MAGIC_I2F
+#define FDSNN_MAGIC_I2F 0  // digit -> double by exponent bits + one DADD instead of I2F.F64
+#endif
 #ifndef FDSNN_RING_S
 #define FDSNN_RING_S 5
 #endif
@@ -100,7 +110,7 @@ template <int M>
 __host__ __device__ constexpr int pbs_stages(int G) { return G >= 6 ? 3 : PbsRing<M>::S; }
 template <int M>
 __host__ __device__ constexpr size_t pbs_smem_bytes(int G, int N, int n, bool ly2 = false) {
-    return 128 + (size_t)pbs_stages<M>(G) * pbs_chunk_bytes<M>() + (size_t)G * pbs_group_bytes<M>(N, n, ly2);
+    return 128 + (size_t)pbs_stages<M>(G) * pbs_chunk_bytes<M>() + (size_t)G * (pbs_group_bytes<M>(N, n, ly2) + PBS_GROUP_PAD);
 }
 
 template <int M>
@@ -193,9 +203,13 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem_raw + 120);
     double2* ring = reinterpret_cast<double2*>(smem_raw + 128);
     const int warp = threadIdx.x / 32;
-    const int g = threadIdx.x / T;
-    const int t = threadIdx.x % T;
-    unsigned char* mine = smem_raw + 128 + S * CHUNK + g * pbs_group_bytes<M>(N, n, LY2);
+    // ILV: groups 2h and 2h+1 share warps 4h..4h+3, lane parity = group, so
+    // the two lanes of a pair hold the same t and their key-slice loads in the
+    // MAC hit one address (a broadcast: half the shared-memory wavefronts).
+    constexpr bool ILV = FDSNN_ILV && M == 512 && G == 4 && PAIR && !LY2;
+    const int g = ILV ? 2 * (threadIdx.x / (2 * T)) + (threadIdx.x & 1) : threadIdx.x / T;
+    const int t = ILV ? (threadIdx.x % (2 * T)) >> 1 : threadIdx.x % T;
+    unsigned char* mine = smem_raw + 128 + S * CHUNK + g * (pbs_group_bytes<M>(N, n, LY2) + PBS_GROUP_PAD);
     double2* buf0 = reinterpret_cast<double2*>(mine);
     double2* buf1 = buf0 + PADM;
     double2* xbuf = buf1 + PADM;  // LY2: warp-local E1 regions (2 x 288)
@@ -211,13 +225,16 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     const int64_t V = (int64_t)args.nlut * args.count;
     const int64_t v0 = args.v_base + (int64_t)blockIdx.x * G;
     const int nact = (int)((V - v0) < G ? (V - v0) : G);  // active groups in this CTA
-    const bool active = g < nact;
+    // ILV runs an odd last group's partner as a shadow of it (same rotation,
+    // no output) so both lanes of every pair take part in the pair barrier.
+    const int nrun = ILV ? ((nact + 1) & ~1) : nact;
+    const bool active = g < nrun;
     const int nchunks = n * 2 * L;  // 32-bit: stage index and phase by constant division
     const bool producer = threadIdx.x == 0;
     if (producer) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], nact * T);
+            mbar_init(&empty[s], nrun * T);
         }
         fence_mbar_init();
     }
@@ -274,8 +291,9 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     // With the phase skew the refills are issued by the last (trailing) group:
     // by the time it releases a stage every leading group has released it too,
     // so the refill never waits on a group that is half a step behind.
-    const bool skewed = PAIR && FDSNN_SKEW && G == 4 && nact > G / 2;
-    const bool refiller = threadIdx.x == (skewed ? (nact - 1) * T : 0);
+    const bool skewed = PAIR && FDSNN_SKEW && G == 4 && nrun > G / 2;
+    const int last_tid = ILV ? 2 * T * ((nrun - 1) / 2) + ((nrun - 1) & 1) : (nact - 1) * T;
+    const bool refiller = threadIdx.x == (skewed ? last_tid : 0);
     auto release = [&](int c) {
         const int s = (int)(c % S);
         mbar_arrive(&empty[s]);
@@ -287,8 +305,8 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     };
 
     if (active) {
-        const int64_t v = v0 + g;
-        const GroupSync gs{1 + g, T};
+        const int64_t v = v0 + (g < nact ? g : nact - 1);
+        const GroupSync gs{ILV ? 1 + g / 2 : 1 + g, ILV ? 2 * T : T};
         const TwiddlesInTmem<M> tw{lane_base};
 
         // ---------------- setup: modulus switch + accumulator init -------------
@@ -356,14 +374,19 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
         // apart -- one in its exchanges while the other runs butterflies.
         const bool lead = g < G / 2;
         auto skew_arrive = [&]() {
-            if (skewed && lead) asm volatile("bar.arrive 15, %0;" ::"r"(T * nact) : "memory");
+            if (skewed && lead) asm volatile("bar.arrive 15, %0;" ::"r"(T * nrun) : "memory");
         };
-        if (skewed && !lead) named_bar(15, T * nact);
+        if (skewed && !lead) named_bar(15, T * nrun);
 
         int c = 0;      // chunk counter = i * 2L + digit
         for (int i = 0; i < n; ++i) {
             const int k = a2N[i];
-            if (k == 0) {  // X^0*ACC - ACC = 0: identity step; keep the key pipeline in sync
+            bool identity = k == 0;
+            // ILV: the pair shares warps (and their barriers, warp-collective
+            // TMEM accesses), so it skips only jointly; a k = 0 step run in
+            // full adds exactly zero (zero digits, zero spectrum, zero rounding).
+            if constexpr (ILV) identity = (k | __shfl_xor_sync(0xffffffffu, k, 1)) == 0;  // every lane shuffles
+            if (identity) {  // X^0*ACC - ACC = 0: identity step; keep the key pipeline in sync
                 for (int d = 0; d < 2 * L; ++d, ++c) {
                     mbar_wait(&full[c % S], (uint32_t)((c / S) & 1));
                     release(c);
@@ -424,6 +447,21 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     {
                         uint32_t twr[32];
                         tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
+#if FDSNN_MAGIC_I2F
+                        // digit fields as doubles without the conversion pipe:
+                        // bits (0x43300000, f) = 2^52 + f, minus (2^52 + B/2 - 1)
+                        const double dmag = 4503599627370496.0 + (double)halfB1;
+                        auto i2d = [&](uint32_t f) { return __hiloint2double(0x43300000, (int)f) - dmag; };
+                        uint32_t d1[8], d2[8], e1[8], e2[8];
+#pragma unroll
+                        for (int r = 0; r < 8; ++r) {
+                            d1[r] = ((uint32_t)xlo[ca][r] >> (bg * la)) & bmask;
+                            d2[r] = ((uint32_t)xhi[ca][r] >> (bg * la)) & bmask;
+                            e1[r] = ((uint32_t)xlo[cb][r] >> (bg * lb)) & bmask;
+                            e2[r] = ((uint32_t)xhi[cb][r] >> (bg * lb)) & bmask;
+                        }
+#else
+                        auto i2d = [](int32_t d) { return (double)d; };
                         int32_t d1[8], d2[8], e1[8], e2[8];
 #pragma unroll
                         for (int r = 0; r < 8; ++r) {
@@ -432,17 +470,18 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                             e1[r] = ((xlo[cb][r] >> (bg * lb)) & bmask) - halfB1;
                             e2[r] = ((xhi[cb][r] >> (bg * lb)) & bmask) - halfB1;
                         }
+#endif
                         tmem_wait32(twr);
 #pragma unroll
                         for (int r = 0; r < 8; ++r) {
                             const double2 tr = words_c(twr, r);
                             if constexpr (FT) {  // twist fused into the first pass
                                 twv[r] = tr;
-                                v0[r] = make_double2((double)d1[r], (double)d2[r]);
-                                v1[r] = make_double2((double)e1[r], (double)e2[r]);
+                                v0[r] = make_double2(i2d(d1[r]), i2d(d2[r]));
+                                v1[r] = make_double2(i2d(e1[r]), i2d(e2[r]));
                             } else {
-                                v0[r] = cmul(make_double2((double)d1[r], (double)d2[r]), tr);
-                                v1[r] = cmul(make_double2((double)e1[r], (double)e2[r]), tr);
+                                v0[r] = cmul(make_double2(i2d(d1[r]), i2d(d2[r])), tr);
+                                v1[r] = cmul(make_double2(i2d(e1[r]), i2d(e2[r])), tr);
                             }
                         }
                     }
@@ -600,7 +639,8 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
             if (args.margin) atomicMax(args.margin, (unsigned long long)__double_as_longlong(err_max));
         }
 
-        if constexpr (MODE_RAW) {
+        if (g >= nact) {  // ILV shadow group: no output
+        } else if constexpr (MODE_RAW) {
             int32_t* a_dst = args.acc_io + v * 2 * N;
             for (int j = t; j < 2 * N; j += T) a_dst[j] = acc[(j >= N ? NA : 0) + ax(j & (N - 1))];
         } else {
