@@ -39,7 +39,7 @@
 #define FDSNN_EARLY_KEYS 1
 #endif
 #ifndef FDSNN_SKEW
-#define FDSNN_SKEW 1  // start half the accumulators of a CTA late: 1 = one transform pair, 2 = ~0.6 pair
+#define FDSNN_SKEW 2  // start half the accumulators of a CTA late: 1 = one transform pair, 2 = ~0.6 pair
 #endif
 #ifndef FDSNN_LY2
 #define FDSNN_LY2 0  // layout-2 transforms (fft2.cuh): bit-exact, 2.5% slower on B200 (DESIGN 8)
