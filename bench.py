@@ -190,7 +190,7 @@ def cpu_oracle_pbs_per_s(neurons_per_core: int = 48):
     return {"value": pbs / compute, "unit": "PBS/s", "cores": cores, "kind": "port",
             "sample": f"{pbs} PBS: fused LIF step (fire+reset, with key switch) on {neurons_per_core} "
                       f"DESK p=1024 neurons per core, {cores} processes, numba+numpy oracle port of "
-                      f"bootstrap.py:517-534 / neuron.py:700-712; timed region excludes keygen; "
+                      f"bootstrap.py:324-341 / neuron.py:160-172; timed region excludes keygen; "
                       f"slowest process of the better of two passes",
             "wall_s": round(wall, 2)}
 

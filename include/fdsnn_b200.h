@@ -20,6 +20,8 @@
  *  - Calls on one context are serialised on the context's CUDA stream unless a
  *    stream is passed explicitly (`*_dev` entry points).
  *  - There is no CPU fallback: without a usable sm_100 device ctx_create fails.
+ *  - No C++ exception crosses this ABI: internal failures (including a
+ *    malformed FDSN container) come back as error codes.
  */
 #ifndef FDSNN_B200_H
 #define FDSNN_B200_H
@@ -62,12 +64,17 @@ void* fdsnn_ctx_stream(fdsnn_ctx* ctx);
 
 /* Load the bootstrapping key and the key-switch key.
  *   rows  : (n, 2l, 2, N) int64 residues — RGSW(s_i) rows [i][row][a|b][coef]
- *           (rgsw.py:141-157 layout, BootstrapKey._ek_fft input bootstrap.py:319-323)
+ *           (rgsw.py:141-157 layout, BootstrapKey._ek_fft input bootstrap.py:125-130)
  *   ksk_A : (N*ks_levels, n) int64, ksk_b : (N*ks_levels,) int64
- *           (KeySwitchKey bootstrap.py:292-303, row index j*levels+i)
+ *           (KeySwitchKey bootstrap.py:99-110, row index j*levels+i)
  * The Fourier transform of the RGSW rows is computed on the device. */
 int fdsnn_bsk_load(fdsnn_ctx* ctx, const int64_t* rows, const int64_t* ksk_A,
                    const int64_t* ksk_b);
+
+/* Load only the key-switch key (bootstrap.key_switch_batch with a standalone
+ * KeySwitchKey, bootstrap.py:303-316): enough for fdsnn_key_switch_batch,
+ * no bootstrapping key is transformed or stored. */
+int fdsnn_ksk_load(fdsnn_ctx* ctx, const int64_t* ksk_A, const int64_t* ksk_b);
 
 /* Load the bootstrapping key straight from a reference "FDSN" BK container
  * (serial.save_bootstrap_key, reference serial.py:111-118): arrays ek_a,
@@ -83,31 +90,31 @@ int fdsnn_ciphertexts_load_fdsn(fdsnn_ctx* ctx, const char* path, const char* pa
                                 int64_t* count, int32_t* ndim, int64_t* shape,
                                 uint32_t* d_rows, void* stream);
 
-/* Register a test polynomial (bootstrap.test_polynomial, bootstrap.py:283-289):
+/* Register a test polynomial (bootstrap.test_polynomial, bootstrap.py:90-96):
  * N int64 residues.  Returns a LUT id usable by the PBS entry points. */
 int fdsnn_lut_load(fdsnn_ctx* ctx, const int64_t* testpoly, int32_t* lut_id);
 
 /* ---- host-buffer entry points (end-to-end; copies inside) ------------- */
 
-/* bootstrap.bootstrap_batch (bootstrap.py:517-534): (count,n),(count,) ->
+/* bootstrap.bootstrap_batch (bootstrap.py:324-341): (count,n),(count,) ->
  * LWE(g(m)) under s, including sample extract and key switch. */
 int fdsnn_pbs_batch(fdsnn_ctx* ctx, int32_t lut_id, const int64_t* A,
                     const int64_t* b, int64_t count, int64_t* outA,
                     int64_t* outb);
 
-/* neuron.fhe_lif_step_batch (neuron.py:700-712): h = v + i; spike2 =
+/* neuron.fhe_lif_step_batch (neuron.py:160-172): h = v + i; spike2 =
  * PBS_fire(h - Delta*v_th_hat) + Delta; v' = PBS_reset(h).  2*count PBS. */
 int fdsnn_lif_step_batch(fdsnn_ctx* ctx, int32_t lut_fire, int32_t lut_reset,
                          int64_t v_th_hat, const int64_t* vA, const int64_t* vb,
                          const int64_t* iA, const int64_t* ib, int64_t count,
                          int64_t* sA, int64_t* sb, int64_t* nA, int64_t* nb);
 
-/* bootstrap.blind_rotate_batch (bootstrap.py:445-475): acc (count,2,N) int64
+/* bootstrap.blind_rotate_batch (bootstrap.py:252-282): acc (count,2,N) int64
  * residues rotated in place by a2N (count,n) residues mod 2N. */
 int fdsnn_blind_rotate_batch(fdsnn_ctx* ctx, int64_t* acc, const int64_t* a2N,
                              int64_t count);
 
-/* bootstrap.key_switch_batch (bootstrap.py:496-509): (count,N),(count,) under
+/* bootstrap.key_switch_batch (bootstrap.py:303-316): (count,N),(count,) under
  * z -> (count,n),(count,) under s. */
 int fdsnn_key_switch_batch(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b,
                            int64_t count, int64_t* outA, int64_t* outb);
@@ -122,7 +129,10 @@ int fdsnn_weight_sum(fdsnn_ctx* ctx, const int64_t* M, int64_t out_cells,
 /* All `rows` pointers are uint32 device arrays of count * fdsnn_row_stride(n)
  * words.  `stream` may be NULL: the legacy default stream. */
 
-/* Host int64 (A,b) -> device rows (with mod-q masking) and back. */
+/* Host int64 (A,b) -> device rows (with mod-q masking) and back.  Rows are
+ * packed/unpacked on the host by a thread pool in page-locked slots that are
+ * DMA'd while the next slot is packed; from_host returns once the host arrays
+ * may be reused, to_host once they are complete.  Thread-safe per context. */
 int fdsnn_rows_from_host(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b,
                          int64_t count, uint32_t* d_rows, void* stream);
 int fdsnn_rows_to_host(fdsnn_ctx* ctx, const uint32_t* d_rows, int64_t count,

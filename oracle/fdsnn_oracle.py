@@ -16,7 +16,7 @@ Arithmetic notes
     (ring.py:103-137): fold+twist, length-M DFT with the e^{+} kernel, MAC in
     the Fourier domain, e^{-} DFT, /M, untwist, round half away from zero.
   * Key switching and weight sums are exact int64 (the reference uses float64
-    GEMMs asserted exact, bootstrap.py:504-508, network.py:416-420).
+    GEMMs asserted exact, bootstrap.py:311-315, network.py:416-420).
 """
 
 from __future__ import annotations
@@ -128,7 +128,7 @@ class OracleKey:
         self.ksk_A = np.asarray(ksk_A, dtype=np.int64)
         self.ksk_b = np.asarray(ksk_b, dtype=np.int64)
         self.tr = Transform(prm["N"])
-        # BootstrapKey._ek_fft (bootstrap.py:319-323)
+        # BootstrapKey._ek_fft (bootstrap.py:125-130)
         self.ek_f = self.tr.forward(center(self.rows, prm["q"]))
 
 
@@ -139,14 +139,14 @@ def params_dict(p):
 
 
 def program_table(pos_values, p):
-    """make_program (bootstrap.py:267-280): antisymmetric fill, centred table."""
+    """make_program (bootstrap.py:74-87): antisymmetric fill, centred table."""
     half = p // 2
     t = np.concatenate([np.asarray(pos_values, np.int64), -np.asarray(pos_values, np.int64)]) % p
     return ((t + half - 1) % p) - (half - 1)
 
 
 def test_polynomial(table, prm):
-    """bootstrap.py:283-289"""
+    """bootstrap.py:90-96"""
     N, p, q = prm["N"], prm["p"], prm["q"]
     slots = (np.arange(N) * p) // (2 * N)
     return ((q // p) * table[slots]) % q
@@ -156,7 +156,7 @@ test_polynomial.__test__ = False
 
 
 def blind_rotate(acc, a2N, key: OracleKey):
-    """GINX CMux chain, numpy restatement of bootstrap.py:362-378 / 445-475."""
+    """GINX CMux chain, numpy restatement of bootstrap.py:169-190 / 445-475."""
     prm = key.prm
     q, N, Bg, l = prm["q"], prm["N"], prm["Bg"], prm["l"]
     acc = np.array(acc, dtype=np.int64)
@@ -178,13 +178,13 @@ def blind_rotate(acc, a2N, key: OracleKey):
 
 
 def sample_extract(acc):
-    """bootstrap.py:484-488"""
+    """bootstrap.py:291-295"""
     a = acc[:, 0, :]
     return np.concatenate([a[:, :1], -a[:, -1:0:-1]], axis=1), acc[:, 1, 0].copy()
 
 
 def key_switch(ea, eb, key: OracleKey):
-    """bootstrap.py:496-509 with exact int64 sums."""
+    """bootstrap.py:303-316 with exact int64 sums."""
     prm = key.prm
     q = prm["q"]
     dig = gadget_decompose(ea, q, prm["ks_base"], prm["ks_l"])  # (B, l, N)
@@ -195,7 +195,7 @@ def key_switch(ea, eb, key: OracleKey):
 
 
 def bootstrap_batch(table, A, b, key: OracleKey):
-    """bootstrap.py:517-534"""
+    """bootstrap.py:324-341"""
     prm = key.prm
     N, p, q = prm["N"], prm["p"], prm["q"]
     a2N = rescale(A, q, 2 * N)
@@ -224,7 +224,7 @@ def reset_table(v_th_hat, leak_num, leak_den, p):
 
 
 def lif_step(vA, vb, iA, ib, v_th_hat, leak_num, leak_den, key: OracleKey):
-    """fhe_lif_step_batch (neuron.py:700-712): charge, fire (+shifts), reset."""
+    """fhe_lif_step_batch (neuron.py:160-172): charge, fire (+shifts), reset."""
     prm = key.prm
     q, p = prm["q"], prm["p"]
     delta = q // p
@@ -237,7 +237,7 @@ def lif_step(vA, vb, iA, ib, v_th_hat, leak_num, leak_den, key: OracleKey):
 
 
 def plain_lif_step(v, i, v_th_hat, leak_num, leak_den):
-    """plain_lif_step_batch (neuron.py:647-659) without the strict range check."""
+    """plain_lif_step_batch (neuron.py:107-119) without the strict range check."""
     h = np.asarray(v, dtype=np.int64) + np.asarray(i, dtype=np.int64)
     fired = h >= v_th_hat
     leak = div_round_half_away(h * leak_num, leak_den)
@@ -351,7 +351,7 @@ def lwe_decrypt(A, b, s, q, p):
 
 # ------------------------------------------------- compiled CPU baseline path
 # The reference accelerates the two elementwise stages of its CMux step with
-# numba (bootstrap.py:386-442).  The CPU-baseline leg of bench.py times the
+# numba (bootstrap.py:193-249).  The CPU-baseline leg of bench.py times the
 # same algorithm with the same library stack, so this module provides numba
 # versions of those two stages (written for this oracle); `blind_rotate_fast`
 # is checked bit-exact against `blind_rotate` in tests/test_oracle_pin.py.
@@ -435,7 +435,7 @@ def blind_rotate_fast(acc, a2N, key: OracleKey):
 
 def key_switch_fast(ea, eb, key: OracleKey):
     """`key_switch` as float64 BLAS products, exact below 2^52 like the
-    reference's own assertion (bootstrap.py:504-508)."""
+    reference's own assertion (bootstrap.py:311-315)."""
     prm = key.prm
     q = prm["q"]
     if not hasattr(key, "_ksk_Af"):

@@ -43,6 +43,7 @@ SIGNATURES = {
     "fdsnn_ctx_destroy": (_c_int, [_vp]),
     "fdsnn_ctx_stream": (_vp, [_vp]),
     "fdsnn_bsk_load": (_c_int, [_vp, _vp, _vp, _vp]),
+    "fdsnn_ksk_load": (_c_int, [_vp, _vp, _vp]),
     "fdsnn_bsk_load_fdsn": (_c_int, [_vp, ctypes.c_char_p, ctypes.c_char_p]),
     "fdsnn_ciphertexts_load_fdsn": (_c_int, [_vp, ctypes.c_char_p, ctypes.c_char_p, _i64p, _i32p,
                                              _i64p, _vp, _vp]),

@@ -2,14 +2,14 @@
 
 Initialize -> BlindRotate -> Extract -> KeySwitch, evaluated on the B200 by
 `csrc/pbs.cuh` + `csrc/keyswitch.cuh` through the C ABI.  Host code here
-builds the lookup tables and test polynomials (bootstrap.py:235-289), runs
-key generation with the reference's RNG order (bootstrap.py:330-348), and
+builds the lookup tables and test polynomials (bootstrap.py:42-96), runs
+key generation with the reference's RNG order (bootstrap.py:137-155), and
 keeps the reference call signatures:
 
-    bootstrap_batch(g, A, b, bsk) -> (A', b')          bootstrap.py:517-534
-    blind_rotate_batch(acc, a2N, bsk) -> acc            bootstrap.py:445-475
-    sample_extract_batch(acc) -> (ea, eb)               bootstrap.py:484-488
-    key_switch_batch(A, b, ksk, params) -> (A', b')     bootstrap.py:496-509
+    bootstrap_batch(g, A, b, bsk) -> (A', b')          bootstrap.py:324-341
+    blind_rotate_batch(acc, a2N, bsk) -> acc            bootstrap.py:252-282
+    sample_extract_batch(acc) -> (ea, eb)               bootstrap.py:291-295
+    key_switch_batch(A, b, ksk, params) -> (A', b')     bootstrap.py:303-316
 
 Outputs are bit-identical to the reference for identical keys and inputs.
 """
@@ -28,7 +28,7 @@ from .ring import monomial_rotate_raw
 
 
 class ProgramFunction:
-    """Negacyclic LUT g: Z_p -> Z_p with g(v + p/2) = -g(v) (bootstrap.py:235-264)."""
+    """Negacyclic LUT g: Z_p -> Z_p with g(v + p/2) = -g(v) (bootstrap.py:42-71)."""
 
     def __init__(self, table, p: int):
         table = np.asarray(table, dtype=np.int64)
@@ -53,7 +53,7 @@ class ProgramFunction:
 
 
 def make_program(g_values, p: int) -> ProgramFunction:
-    """LUT from values on [0, p/2); negative half by antisymmetry (bootstrap.py:267-280)."""
+    """LUT from values on [0, p/2); negative half by antisymmetry (bootstrap.py:74-87)."""
     half = p // 2
     get = g_values if callable(g_values) else g_values.__getitem__
     pos = np.array([int(get(v)) for v in range(half)], dtype=np.int64)
@@ -61,7 +61,7 @@ def make_program(g_values, p: int) -> ProgramFunction:
 
 
 def test_polynomial(g: ProgramFunction, params: FheParams) -> np.ndarray:
-    """v_i = Delta * g(floor(i*p/2N)) mod q (bootstrap.py:283-289)."""
+    """v_i = Delta * g(floor(i*p/2N)) mod q (bootstrap.py:90-96)."""
     if g.p != params.p:
         raise ParameterError("program function is for a different message modulus")
     slots = (np.arange(params.N, dtype=np.int64) * params.p) // (2 * params.N)
@@ -73,7 +73,7 @@ test_polynomial.__test__ = False  # not a pytest test
 
 @dataclass(frozen=True)
 class KeySwitchKey:
-    """LWE encryptions of z_j*base^i under s, row j*levels+i (bootstrap.py:292-303)."""
+    """LWE encryptions of z_j*base^i under s, row j*levels+i (bootstrap.py:99-110)."""
 
     A: np.ndarray  # (N*levels, n)
     b: np.ndarray  # (N*levels,)
@@ -122,6 +122,7 @@ class BootstrapKey:
             ctx = DeviceContext(self.params)
             ctx.load_keys(self.rows, self.ksk.A, self.ksk.b)
             self._device = ctx
+            _register_ks_device(self.ksk, self.params, ctx)
         return self._device
 
     def __getstate__(self):
@@ -132,7 +133,7 @@ class BootstrapKey:
 
 def gen_key_switch_key(zk: RlweSecretKey, sk: LweSecretKey, params: FheParams,
                        rng: np.random.Generator) -> KeySwitchKey:
-    """RNG order as bootstrap.py:330-341: mask grid draw, noise draw."""
+    """RNG order as bootstrap.py:137-148: mask grid draw, noise draw."""
     N, n = params.N, params.n
     base, levels = params.ks_base, params.ks_levels
     count = N * levels
@@ -146,14 +147,14 @@ def gen_key_switch_key(zk: RlweSecretKey, sk: LweSecretKey, params: FheParams,
 
 def gen_bootstrap_key(sk: LweSecretKey, zk: RlweSecretKey, params: FheParams,
                       rng: np.random.Generator) -> BootstrapKey:
-    """n RGSW bit encryptions then the KSK, in the reference's order (bootstrap.py:344-348)."""
+    """n RGSW bit encryptions then the KSK, in the reference's order (bootstrap.py:151-155)."""
     ek = [rgsw_encrypt_bit(int(s_i), zk, params, rng) for s_i in sk.s]
     ksk = gen_key_switch_key(zk, sk, params, rng)
     return BootstrapKey(ek, ksk, params)
 
 
 def initialize_accumulator(g: ProgramFunction, b2N: int, params: FheParams) -> RlweCiphertext:
-    """Noiseless RLWE of X^{-b2N} * testpoly(g) (bootstrap.py:351-355)."""
+    """Noiseless RLWE of X^{-b2N} * testpoly(g) (bootstrap.py:158-166)."""
     v = test_polynomial(g, params)
     rotated = monomial_rotate_raw(v, -int(b2N) % (2 * params.N), params.N)
     return RlweCiphertext(np.zeros(params.N, dtype=np.int64), rotated, params.q)
@@ -175,12 +176,24 @@ def _device_of(bsk):
 
 
 def blind_rotate_batch(acc: np.ndarray, a2N: np.ndarray, bsk) -> np.ndarray:
-    """Rotate (B,2,N) accumulators by the encrypted phases a2N (B,n) (bootstrap.py:445-475)."""
+    """Rotate (B,2,N) accumulators by the encrypted phases a2N (B,n) (bootstrap.py:252-282).
+
+    Same ownership as the reference: `acc` goes through np.ascontiguousarray,
+    so a C-contiguous int64 array is rotated in place and returned (the
+    reference's numba kernels write into it, bootstrap.py:263,281); any other
+    array is copied first.  When no step rotates anything (every a2N entry is
+    0 mod 2N: the reference skips every step, bootstrap.py:274-276) the
+    accumulators come back untouched, unreduced values included.
+    """
     params = bsk.params
-    acc = np.asarray(acc, dtype=np.int64)
+    acc = np.ascontiguousarray(acc)
     a2N = np.asarray(a2N, dtype=np.int64)
     if acc.ndim != 3 or acc.shape[1:] != (2, params.N) or a2N.shape != (acc.shape[0], params.n):
         raise ParameterError("accumulator / rotation shapes do not match params")
+    if not (a2N % (2 * params.N)).any():
+        return acc
+    if acc.dtype != np.int64 or not acc.flags.writeable:
+        acc = acc.astype(np.int64)
     return _device_of(bsk).blind_rotate_batch(acc, a2N)
 
 
@@ -191,7 +204,7 @@ def blind_rotate(acc: RlweCiphertext, a2N, bsk) -> RlweCiphertext:
 
 
 def sample_extract_batch(acc: np.ndarray):
-    """(B,2,N) -> LWE under z: (a_0, -a_{N-1}, ..., -a_1), b = body_0 (bootstrap.py:484-488).
+    """(B,2,N) -> LWE under z: (a_0, -a_{N-1}, ..., -a_1), b = body_0 (bootstrap.py:291-295).
 
     Pure index permutation of host arrays (the device path fuses it into the
     blind-rotation epilogue).
@@ -207,24 +220,47 @@ def sample_extract(acc: RlweCiphertext) -> LweCiphertext:
     return LweCiphertext(ea[0], int(eb[0]), acc.q)
 
 
-def _key_device(ksk: KeySwitchKey, params: FheParams):
-    cache = _KS_DEVICES.get(id(ksk))
-    if cache is not None and cache[0] is ksk:
-        return cache[1]
-    from .device import DeviceContext
-    dev = DeviceContext(params)
-    zero_rows = np.zeros((params.n, 2 * params.gadget.levels, 2, params.N), dtype=np.int64)
-    dev.load_keys(zero_rows, ksk.A, ksk.b)
-    _KS_DEVICES[id(ksk)] = (ksk, dev)
-    return dev
-
-
+# Device contexts able to key-switch with a given KeySwitchKey, keyed by
+# (id(ksk), params digest).  A bootstrapping key's context registers its own
+# key-switch key when it is created, so key_switch_batch(..., bsk.ksk, ...)
+# reuses it; a standalone key gets a context holding only the key-switch key.
+# Entries die with their key (weakref.finalize), so nothing accumulates.
 _KS_DEVICES: dict = {}
+
+
+def _register_ks_device(ksk, params: FheParams, ctx) -> None:
+    import weakref
+    key = (id(ksk), params.digest())
+    if key in _KS_DEVICES:
+        return
+    try:
+        ref = weakref.ref(ksk)
+    except TypeError:  # not weak-referenceable: do not cache
+        return
+    _KS_DEVICES[key] = (ref, weakref.ref(ctx))
+    weakref.finalize(ksk, _KS_DEVICES.pop, key, None)
+
+
+def _key_device(ksk: KeySwitchKey, params: FheParams):
+    hit = _KS_DEVICES.get((id(ksk), params.digest()))
+    if hit is not None and hit[0]() is ksk:
+        ctx = hit[1]()
+        if ctx is not None and getattr(ctx, "h", None):
+            return ctx
+        _KS_DEVICES.pop((id(ksk), params.digest()), None)
+    from .device import DeviceContext
+    ctx = DeviceContext(params)
+    ctx.load_key_switch_key(ksk.A, ksk.b)
+    ksk_ctxs = getattr(ksk, "__dict__", None)
+    if ksk_ctxs is not None:  # the key owns its standalone context (frozen dataclass: bypass setattr)
+        object.__setattr__(ksk, "_b200_ks_ctx", ctx)
+    _register_ks_device(ksk, params, ctx)
+    return ctx
 
 
 def key_switch_batch(A: np.ndarray, b: np.ndarray, ksk: KeySwitchKey,
                      params: FheParams):
-    """LWE under z (dim N) -> LWE under s (dim n) on the device (bootstrap.py:496-509)."""
+    """LWE under z (dim N) -> LWE under s (dim n) on the device (bootstrap.py:303-316)."""
     A = np.asarray(A, dtype=np.int64)
     if A.shape[-1] != ksk.N:
         raise ParameterError("ciphertext dimension does not match key-switch key")
@@ -239,7 +275,7 @@ def key_switch(ct: LweCiphertext, ksk: KeySwitchKey, params: FheParams) -> LweCi
 
 
 def bootstrap_batch(g: ProgramFunction, A: np.ndarray, b: np.ndarray, bsk):
-    """LWE(m) -> LWE(g(m)) for a batch, on the B200 (bootstrap.py:517-534)."""
+    """LWE(m) -> LWE(g(m)) for a batch, on the B200 (bootstrap.py:324-341)."""
     params = bsk.params
     A = np.asarray(A, dtype=np.int64)
     b = np.asarray(b, dtype=np.int64)

@@ -16,6 +16,7 @@
 
 #include "../../include/fdsnn_b200.h"
 #include "fdsn.h"
+#include "hostio.h"
 #include "keyswitch.cuh"
 #include "ks_umma.cuh"
 #include "linear.cuh"
@@ -100,14 +101,17 @@ struct fdsnn_ctx {
     int ks_limbs = 0, ks_ksteps = 0, ks_ntiles = 0;
     // Per-stream scratch of the PBS pipeline (extracted z-LWE rows, key-switch
     // digit tiles), so launches on different streams never share buffers.
-    struct StreamScratch { Buf ext, ks_dig; };
+    // `stage`: device staging of the client-side encrypt/decrypt entry points;
+    // `pin`: page-locked slots of the int64 host boundary (hostio.h).
+    struct StreamScratch { Buf ext, ks_dig, stage; PinnedSlots pin; };
     std::map<cudaStream_t, StreamScratch> scratch;
     int64_t wide_max = 148;  // largest batch routed to the latency kernel (FDSNN_WIDE_MAX)
     int64_t sm_count = 148;
-    bool keys_loaded = false;
+    bool keys_loaded = false;  // bootstrapping key (and its key-switch key)
+    bool ks_loaded = false;    // key-switch key
     std::vector<int32_t*> luts;
     std::vector<Operator> ops;
-    Buf ext, rows_a, rows_b, rows_c, host_stage, acc_buf, a2n_buf, l2flush;
+    Buf ext, rows_a, rows_b, rows_c, acc_buf, a2n_buf, l2flush;
     unsigned long long* margin = nullptr;
     bool track_margin = false;
     bool timing = false;
@@ -150,7 +154,7 @@ cudaStream_t pick(fdsnn_ctx* ctx, void* stream) {
 // V = rotations covered by this launch, starting at a.v_base
 template <int M, int G, bool RAW, bool MARGIN, bool PAIR, int LQ = 2>
 int launch_br_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_t s) {
-    const size_t smem = pbs_smem_bytes<M>(G, 2 * M, ctx->dp.n, PAIR && M == 512 && FDSNN_LY2);
+    const size_t smem = pbs_smem_bytes<M>(G, 2 * M, ctx->dp.n);
     auto kern = pbs_blind_rotate_kernel<M, G, RAW, MARGIN, PAIR, LQ>;
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (V + G - 1) / G;
@@ -215,9 +219,8 @@ int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_
             return launch_br_m<512, 1>(ctx, a, V, raw, s);
         case 1024: {
             // C4 (l = 3): the six digit transforms of a step in three
-            // pipelined pairs (FDSNN_C4PAIR=0: one at a time)
-            static const bool pair3 = !(getenv("FDSNN_C4PAIR") && atoi(getenv("FDSNN_C4PAIR")) == 0);
-            if (pair3 && ctx->dp.L == 3) return launch_br_m<1024, 2, true, 3>(ctx, a, V, raw, s);
+            // pipelined pairs
+            if (ctx->dp.L == 3) return launch_br_m<1024, 2, true, 3>(ctx, a, V, raw, s);
             return launch_br_m<1024, 2>(ctx, a, V, raw, s);
         }
     }
@@ -383,6 +386,27 @@ int pbs_pipeline(fdsnn_ctx* ctx, int nlut, const int32_t* lut_ids, const int64_t
     return launch_ks(ctx, k, s);
 }
 
+// KSK: (N*ks_L) x stride uint32 [A | b | 0], its body column, and the
+// tensor-core limb tiles.  Caller holds ctx->mu.
+int load_ksk_impl(fdsnn_ctx* ctx, const int64_t* ksk_A, const int64_t* ksk_b) {
+    const DevParams& d = ctx->dp;
+    const int64_t krows = (int64_t)d.N * d.ks_L;
+    std::vector<uint32_t> kh((size_t)krows * d.stride, 0u);
+    for (int64_t r = 0; r < krows; ++r) {
+        for (int c = 0; c < d.n; ++c) kh[r * d.stride + c] = (uint32_t)ksk_A[r * d.n + c] & d.qmask;
+        kh[r * d.stride + d.n] = (uint32_t)ksk_b[r] & d.qmask;
+    }
+    if (!ctx->ksk) CU(cudaMalloc(&ctx->ksk, kh.size() * 4));
+    CU(cudaMemcpyAsync(ctx->ksk, kh.data(), kh.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<uint32_t> kb((size_t)krows);
+    for (int64_t r = 0; r < krows; ++r) kb[r] = kh[r * d.stride + d.n];
+    if (!ctx->kskb) CU(cudaMalloc(&ctx->kskb, kb.size() * 4));
+    CU(cudaMemcpyAsync(ctx->kskb, kb.data(), kb.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (int rc = prepare_ks_umma(ctx)) return rc;
+    CU(cudaStreamSynchronize(ctx->stream));
+    return FDSNN_OK;
+}
+
 __global__ void fp64_peak_kernel(double* out, int iters) {
     double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
     double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
@@ -398,6 +422,42 @@ __global__ void fp64_peak_kernel(double* out, int iters) {
     if (s == 12345.678) out[0] = s;  // never true; keeps the chain live
 }
 
+// Every extern "C" entry point runs its body through guarded(): no C++
+// exception (bad_alloc from a hostile FDSN extent, a std::map insert, ...)
+// may cross the C ABI into the caller's process.
+template <class F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const std::bad_alloc&) {
+        return set_err(FDSNN_ERR_PARAMETER, "host allocation failed");
+    } catch (const std::exception& e) {
+        return set_err(FDSNN_ERR_STATE, "internal error: %s", e.what());
+    } catch (...) {
+        return set_err(FDSNN_ERR_STATE, "internal error");
+    }
+}
+
+// int64 host arrays <-> device rows through the calling stream's pinned slots
+// (hostio.h).  Callers hold ctx->mu (the per-stream scratch map is shared).
+int rows_from_host_impl(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b, int64_t count, uint32_t* d_rows,
+                        cudaStream_t s) {
+    if (count <= 0) return FDSNN_OK;
+    if (!A || !b || !d_rows) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+    const DevParams& d = ctx->dp;
+    CU(upload_rows(ctx->scratch[s].pin, A, b, count, d.n, d.stride, d.qmask, d_rows, s));
+    return FDSNN_OK;
+}
+
+int rows_to_host_impl(fdsnn_ctx* ctx, const uint32_t* d_rows, int64_t count, int64_t* A, int64_t* b,
+                      cudaStream_t s) {
+    if (count <= 0) return FDSNN_OK;
+    if (!A || !b || !d_rows) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+    const DevParams& d = ctx->dp;
+    CU(download_rows(ctx->scratch[s].pin, d_rows, count, d.n, d.stride, A, b, s));
+    return FDSNN_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -407,259 +467,273 @@ const char* fdsnn_last_error(void) { return g_last_error.c_str(); }
 int32_t fdsnn_row_stride(int32_t n) { return round4(n + 1); }
 
 int fdsnn_ctx_create(const fdsnn_params* prm, int32_t device, fdsnn_ctx** out) {
-    if (!prm || !out) return set_err(FDSNN_ERR_PARAMETER, "null argument");
-    const fdsnn_params& p = *prm;
-    if (!(p.N == 512 || p.N == 1024 || p.N == 2048))
-        return set_err(FDSNN_ERR_PARAMETER, "ring degree N=%d not supported (512, 1024, 2048)", p.N);
-    if (p.log2_q < 2 || p.log2_q > 31) return set_err(FDSNN_ERR_PARAMETER, "q must be 2^k with 2<=k<=31");
-    if (!is_pow2(p.p) || p.p % 2 || p.p > 2 * p.N) return set_err(FDSNN_ERR_PARAMETER, "bad message modulus p=%d", p.p);
-    if (p.n < 1 || p.n > 2048) return set_err(FDSNN_ERR_PARAMETER, "LWE dimension n=%d out of range", p.n);
-    if (p.bg_log < 1 || p.levels < 1 || p.bg_log * p.levels < p.log2_q)
-        return set_err(FDSNN_ERR_PARAMETER, "gadget must cover q (base**levels >= q)");
-    if (p.ks_log < 1 || p.ks_levels < 1 || p.ks_log * p.ks_levels < p.log2_q)
-        return set_err(FDSNN_ERR_PARAMETER, "key-switch gadget must cover q");
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-        return set_err(FDSNN_ERR_CUDA, "no CUDA device available (this library has no CPU fallback)");
-    if (device < 0 || device >= ndev) return set_err(FDSNN_ERR_PARAMETER, "bad device %d", device);
-    cudaDeviceProp dprop;
-    CU(cudaGetDeviceProperties(&dprop, device));
-    if (dprop.major != 10) return set_err(FDSNN_ERR_CUDA, "device %s is sm_%d%d; this build targets sm_100a", dprop.name, dprop.major, dprop.minor);
-    CU(cudaSetDevice(device));
-    fdsnn_ctx* ctx = new fdsnn_ctx();
-    ctx->prm = p;
-    ctx->device = device;
-    ctx->wide_max = dprop.multiProcessorCount;
-    ctx->sm_count = dprop.multiProcessorCount;
-    if (const char* e = getenv("FDSNN_WIDE_MAX")) ctx->wide_max = atoll(e);
-    DevParams& d = ctx->dp;
-    d.n = p.n;
-    d.N = p.N;
-    d.M = p.N / 2;
-    d.log2q = p.log2_q;
-    d.qmask = (uint32_t)((1ull << p.log2_q) - 1);
-    d.bg_log = p.bg_log;
-    d.L = p.levels;
-    d.ks_log = p.ks_log;
-    d.ks_L = p.ks_levels;
-    d.stride = round4(p.n + 1);
-    d.ext_stride = round4(p.N + 1);
-    d.p = p.p;
-    d.half_slot = p.N / p.p;
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
-        delete ctx;
-        return set_err(FDSNN_ERR_CUDA, "stream creation failed");
-    }
-    // transform tables in long double (ring.py:115-118):
-    //   twist[j] = e^{i pi j/N}, j < M, then the interior-pass twiddles
-    //   e^{2 pi i r jm/(NS R)} in the fft.cuh layout [pass][r-1][jm].
-    const int M = d.M;
-    const long double PI = 3.141592653589793238462643383279502884L;
-    std::vector<double2> tab(M);
-    for (int k = 0; k < M; ++k) {
-        long double tw = PI * k / p.N;
-        tab[k] = make_double2((double)cosl(tw), (double)sinl(tw));
-    }
-    {
-        // M = 1024 runs as two 512-point transforms (fft.cuh parity split):
-        // the M = 512 pass twiddles, then the radix-2 join factors below
-        const int* radix = M == 256 ? Schedule<256>::R : Schedule<512>::R;
-        const int P = 3;
-        int ns = radix[0];
-        for (int pass = 1; pass < P; ++pass) {
-            const int R = radix[pass];
-            for (int r = 1; r < R; ++r)
-                for (int jm = 0; jm < ns; ++jm) {
-                    long double ang = 2.0L * PI * r * jm / ((long double)ns * R);
+    return guarded([&]() -> int {
+        if (!prm || !out) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        const fdsnn_params& p = *prm;
+        if (!(p.N == 512 || p.N == 1024 || p.N == 2048))
+            return set_err(FDSNN_ERR_PARAMETER, "ring degree N=%d not supported (512, 1024, 2048)", p.N);
+        if (p.log2_q < 2 || p.log2_q > 31) return set_err(FDSNN_ERR_PARAMETER, "q must be 2^k with 2<=k<=31");
+        if (!is_pow2(p.p) || p.p % 2 || p.p > 2 * p.N) return set_err(FDSNN_ERR_PARAMETER, "bad message modulus p=%d", p.p);
+        if (p.n < 1 || p.n > 2048) return set_err(FDSNN_ERR_PARAMETER, "LWE dimension n=%d out of range", p.n);
+        if (p.bg_log < 1 || p.levels < 1 || p.bg_log * p.levels < p.log2_q)
+            return set_err(FDSNN_ERR_PARAMETER, "gadget must cover q (base**levels >= q)");
+        if (p.ks_log < 1 || p.ks_levels < 1 || p.ks_log * p.ks_levels < p.log2_q)
+            return set_err(FDSNN_ERR_PARAMETER, "key-switch gadget must cover q");
+        // The rotation kernels extract the signed gadget digits from
+        // y = centred(x) + H, H = (B/2-1)(1 + B + ... + B^(l-1)), in int32
+        // (pbs.cuh): y must fit, and so must the key-switch digit recursion.
+        {
+            if (p.bg_log > 30 || (int64_t)p.bg_log * (p.levels - 1) > 62)
+                return set_err(FDSNN_ERR_PARAMETER, "gadget base 2^%d with %d levels is outside the int32 digit range",
+                               p.bg_log, p.levels);
+            int64_t hsum = 0;
+            for (int lvl = 0; lvl < p.levels; ++lvl) hsum += ((1ll << (p.bg_log - 1)) - 1) << (p.bg_log * lvl);
+            const int64_t halfq = 1ll << (p.log2_q - 1);
+            if (hsum + halfq > INT32_MAX || hsum - halfq < INT32_MIN)
+                return set_err(FDSNN_ERR_PARAMETER,
+                               "gadget base 2^%d with %d levels at q=2^%d is outside the int32 digit range",
+                               p.bg_log, p.levels, p.log2_q);
+            if (p.ks_log > 30) return set_err(FDSNN_ERR_PARAMETER, "key-switch base 2^%d too large", p.ks_log);
+        }
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            return set_err(FDSNN_ERR_CUDA, "no CUDA device available (this library has no CPU fallback)");
+        if (device < 0 || device >= ndev) return set_err(FDSNN_ERR_PARAMETER, "bad device %d", device);
+        cudaDeviceProp dprop;
+        CU(cudaGetDeviceProperties(&dprop, device));
+        if (dprop.major != 10) return set_err(FDSNN_ERR_CUDA, "device %s is sm_%d%d; this build targets sm_100a", dprop.name, dprop.major, dprop.minor);
+        CU(cudaSetDevice(device));
+        fdsnn_ctx* ctx = new fdsnn_ctx();
+        ctx->prm = p;
+        ctx->device = device;
+        ctx->wide_max = dprop.multiProcessorCount;
+        ctx->sm_count = dprop.multiProcessorCount;
+        if (const char* e = getenv("FDSNN_WIDE_MAX")) ctx->wide_max = atoll(e);
+        DevParams& d = ctx->dp;
+        d.n = p.n;
+        d.N = p.N;
+        d.M = p.N / 2;
+        d.log2q = p.log2_q;
+        d.qmask = (uint32_t)((1ull << p.log2_q) - 1);
+        d.bg_log = p.bg_log;
+        d.L = p.levels;
+        d.ks_log = p.ks_log;
+        d.ks_L = p.ks_levels;
+        d.stride = round4(p.n + 1);
+        d.ext_stride = round4(p.N + 1);
+        d.p = p.p;
+        d.half_slot = p.N / p.p;
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete ctx;
+            return set_err(FDSNN_ERR_CUDA, "stream creation failed");
+        }
+        // transform tables in long double (ring.py:115-118):
+        //   twist[j] = e^{i pi j/N}, j < M, then the interior-pass twiddles
+        //   e^{2 pi i r jm/(NS R)} in the fft.cuh layout [pass][r-1][jm].
+        const int M = d.M;
+        const long double PI = 3.141592653589793238462643383279502884L;
+        std::vector<double2> tab(M);
+        for (int k = 0; k < M; ++k) {
+            long double tw = PI * k / p.N;
+            tab[k] = make_double2((double)cosl(tw), (double)sinl(tw));
+        }
+        {
+            // M = 1024 runs as two 512-point transforms (fft.cuh parity split):
+            // the M = 512 pass twiddles, then the radix-2 join factors below
+            const int* radix = M == 256 ? Schedule<256>::R : Schedule<512>::R;
+            const int P = 3;
+            int ns = radix[0];
+            for (int pass = 1; pass < P; ++pass) {
+                const int R = radix[pass];
+                for (int r = 1; r < R; ++r)
+                    for (int jm = 0; jm < ns; ++jm) {
+                        long double ang = 2.0L * PI * r * jm / ((long double)ns * R);
+                        tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+                    }
+                ns *= R;
+            }
+            if (M == 1024)
+                for (int k = 0; k < 512; ++k) {
+                    long double ang = 2.0L * PI * k / 1024.0L;
                     tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
                 }
-            ns *= R;
         }
-        if (M == 512) {  // layout-2 transform twiddles (fft2.cuh): w64^m, w512^m
-            for (int m = 0; m < 64; ++m) {
-                long double ang = 2.0L * PI * m / 64.0L;
-                tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
-            }
-            for (int m = 0; m < 512; ++m) {
-                long double ang = 2.0L * PI * m / 512.0L;
-                tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
-            }
+        if (cudaMalloc(&ctx->tables, tab.size() * sizeof(double2)) != cudaSuccess ||
+            cudaMemcpy(ctx->tables, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMalloc(&ctx->margin, sizeof(unsigned long long)) != cudaSuccess ||
+            cudaMemset(ctx->margin, 0, sizeof(unsigned long long)) != cudaSuccess) {
+            fdsnn_ctx_destroy(ctx);
+            return set_err(FDSNN_ERR_CUDA, "device allocation failed");
         }
-        if (M == 1024)
-            for (int k = 0; k < 512; ++k) {
-                long double ang = 2.0L * PI * k / 1024.0L;
-                tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
-            }
-    }
-    if (cudaMalloc(&ctx->tables, tab.size() * sizeof(double2)) != cudaSuccess ||
-        cudaMemcpy(ctx->tables, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMalloc(&ctx->margin, sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMemset(ctx->margin, 0, sizeof(unsigned long long)) != cudaSuccess) {
-        fdsnn_ctx_destroy(ctx);
-        return set_err(FDSNN_ERR_CUDA, "device allocation failed");
-    }
-    *out = ctx;
-    return FDSNN_OK;
+        *out = ctx;
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_ctx_destroy(fdsnn_ctx* ctx) {
-    if (!ctx) return FDSNN_OK;
-    cudaSetDevice(ctx->device);
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    for (auto& t : ctx->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
-    for (auto* l : ctx->luts) cudaFree(l);
-    for (auto& o : ctx->ops) { cudaFree(o.w); cudaFree(o.row_ptr); cudaFree(o.col_idx); cudaFree(o.val); }
-    cudaFree(ctx->tables);
-    cudaFree(ctx->bsk);
-    cudaFree(ctx->ksk);
-    cudaFree(ctx->kskb);
-    cudaFree(ctx->ks_bt);
-    for (auto& kv : ctx->scratch) { kv.second.ext.release(); kv.second.ks_dig.release(); }
-    cudaFree(ctx->margin);
-    ctx->ext.release(); ctx->rows_a.release(); ctx->rows_b.release(); ctx->rows_c.release();
-    ctx->host_stage.release(); ctx->acc_buf.release(); ctx->a2n_buf.release(); ctx->l2flush.release();
-    if (ctx->stream) cudaStreamDestroy(ctx->stream);
-    delete ctx;
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return FDSNN_OK;
+        cudaSetDevice(ctx->device);
+        if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+        for (auto& t : ctx->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+        for (auto* l : ctx->luts) cudaFree(l);
+        for (auto& o : ctx->ops) { cudaFree(o.w); cudaFree(o.row_ptr); cudaFree(o.col_idx); cudaFree(o.val); }
+        cudaFree(ctx->tables);
+        cudaFree(ctx->bsk);
+        cudaFree(ctx->ksk);
+        cudaFree(ctx->kskb);
+        cudaFree(ctx->ks_bt);
+        for (auto& kv : ctx->scratch) {
+            kv.second.ext.release();
+            kv.second.ks_dig.release();
+            kv.second.stage.release();
+            kv.second.pin.release();
+        }
+        cudaFree(ctx->margin);
+        ctx->ext.release(); ctx->rows_a.release(); ctx->rows_b.release(); ctx->rows_c.release();
+        ctx->acc_buf.release(); ctx->a2n_buf.release(); ctx->l2flush.release();
+        if (ctx->stream) cudaStreamDestroy(ctx->stream);
+        delete ctx;
+        return FDSNN_OK;
+    });
 }
 
 void* fdsnn_ctx_stream(fdsnn_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 int fdsnn_bsk_load(fdsnn_ctx* ctx, const int64_t* rows, const int64_t* ksk_A, const int64_t* ksk_b) {
-    if (!ctx || !rows || !ksk_A || !ksk_b) return set_err(FDSNN_ERR_PARAMETER, "null argument");
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    CU(cudaSetDevice(ctx->device));
-    const DevParams& d = ctx->dp;
-    const int64_t npoly = (int64_t)d.n * 2 * d.L * 2;
-    const size_t row_bytes = (size_t)npoly * d.N * sizeof(int64_t);
-    int64_t* d_rows = nullptr;
-    CU(cudaMalloc(&d_rows, row_bytes));
-    CU(cudaMemcpyAsync(d_rows, rows, row_bytes, cudaMemcpyHostToDevice, ctx->stream));
-    if (!ctx->bsk) CU(cudaMalloc(&ctx->bsk, (size_t)npoly * d.M * sizeof(double2)));
-    {
-        const int M = d.M;
-        const int T = M / 8;
-        const int G = 128 / T > 0 ? 128 / T : 1;
-        const size_t padm = M == 1024 ? PbsShape<1024>::PADM : M == 512 ? PbsShape<512>::PADM : PbsShape<256>::PADM;
-        const size_t smem = (size_t)G * 2 * padm * sizeof(double2);
-        const unsigned blocks = (unsigned)((npoly + G - 1) / G);
-        switch (M) {
-            case 256:
-                CU(cudaFuncSetAttribute(bsk_forward_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                bsk_forward_kernel<256, 4><<<blocks, 128, smem, ctx->stream>>>(d_rows, npoly, d.log2q, ctx->tables, ctx->bsk);
-                break;
-            case 512:
-                CU(cudaFuncSetAttribute(bsk_forward_kernel<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                bsk_forward_kernel<512, 2><<<blocks, 128, smem, ctx->stream>>>(d_rows, npoly, d.log2q, ctx->tables, ctx->bsk);
-                break;
-            case 1024:
-                CU(cudaFuncSetAttribute(bsk_forward_kernel<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                bsk_forward_kernel<1024, 1><<<blocks, 128, smem, ctx->stream>>>(d_rows, npoly, d.log2q, ctx->tables, ctx->bsk);
-                break;
+    return guarded([&]() -> int {
+        if (!ctx || !rows || !ksk_A || !ksk_b) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        const DevParams& d = ctx->dp;
+        const int64_t npoly = (int64_t)d.n * 2 * d.L * 2;
+        const size_t row_bytes = (size_t)npoly * d.N * sizeof(int64_t);
+        int64_t* d_rows = nullptr;
+        CU(cudaMalloc(&d_rows, row_bytes));
+        CU(cudaMemcpyAsync(d_rows, rows, row_bytes, cudaMemcpyHostToDevice, ctx->stream));
+        if (!ctx->bsk) CU(cudaMalloc(&ctx->bsk, (size_t)npoly * d.M * sizeof(double2)));
+        {
+            const int M = d.M;
+            const int T = M / 8;
+            const int G = 128 / T > 0 ? 128 / T : 1;
+            const size_t padm = M == 1024 ? PbsShape<1024>::PADM : M == 512 ? PbsShape<512>::PADM : PbsShape<256>::PADM;
+            const size_t smem = (size_t)G * 2 * padm * sizeof(double2);
+            const unsigned blocks = (unsigned)((npoly + G - 1) / G);
+            switch (M) {
+                case 256:
+                    CU(cudaFuncSetAttribute(bsk_forward_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    bsk_forward_kernel<256, 4><<<blocks, 128, smem, ctx->stream>>>(d_rows, npoly, d.log2q, ctx->tables, ctx->bsk);
+                    break;
+                case 512:
+                    CU(cudaFuncSetAttribute(bsk_forward_kernel<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    bsk_forward_kernel<512, 2><<<blocks, 128, smem, ctx->stream>>>(d_rows, npoly, d.log2q, ctx->tables, ctx->bsk);
+                    break;
+                case 1024:
+                    CU(cudaFuncSetAttribute(bsk_forward_kernel<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    bsk_forward_kernel<1024, 1><<<blocks, 128, smem, ctx->stream>>>(d_rows, npoly, d.log2q, ctx->tables, ctx->bsk);
+                    break;
+            }
+            CU(cudaGetLastError());
         }
-        CU(cudaGetLastError());
-    }
-    // KSK: (N*ks_L) x stride uint32 [A | b | 0]
-    const int64_t krows = (int64_t)d.N * d.ks_L;
-    std::vector<uint32_t> kh((size_t)krows * d.stride, 0u);
-    for (int64_t r = 0; r < krows; ++r) {
-        for (int c = 0; c < d.n; ++c) kh[r * d.stride + c] = (uint32_t)ksk_A[r * d.n + c] & d.qmask;
-        kh[r * d.stride + d.n] = (uint32_t)ksk_b[r] & d.qmask;
-    }
-    if (!ctx->ksk) CU(cudaMalloc(&ctx->ksk, kh.size() * 4));
-    CU(cudaMemcpyAsync(ctx->ksk, kh.data(), kh.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-    std::vector<uint32_t> kb((size_t)krows);
-    for (int64_t r = 0; r < krows; ++r) kb[r] = kh[r * d.stride + d.n];
-    if (!ctx->kskb) CU(cudaMalloc(&ctx->kskb, kb.size() * 4));
-    CU(cudaMemcpyAsync(ctx->kskb, kb.data(), kb.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-    {
-        int rc = prepare_ks_umma(ctx);
-        if (rc) return rc;
-    }
-    CU(cudaStreamSynchronize(ctx->stream));
-    CU(cudaFree(d_rows));
-    ctx->keys_loaded = true;
-    return FDSNN_OK;
+        if (int rc = load_ksk_impl(ctx, ksk_A, ksk_b)) return rc;
+        CU(cudaStreamSynchronize(ctx->stream));
+        CU(cudaFree(d_rows));
+        ctx->keys_loaded = true;
+        ctx->ks_loaded = true;
+        return FDSNN_OK;
+    });
+}
+
+int fdsnn_ksk_load(fdsnn_ctx* ctx, const int64_t* ksk_A, const int64_t* ksk_b) {
+    return guarded([&]() -> int {
+        if (!ctx || !ksk_A || !ksk_b) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        if (int rc = load_ksk_impl(ctx, ksk_A, ksk_b)) return rc;
+        ctx->ks_loaded = true;
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_bsk_load_fdsn(fdsnn_ctx* ctx, const char* path, const char* params_digest) {
-    if (!ctx || !path) return set_err(FDSNN_ERR_PARAMETER, "null argument");
-    std::map<std::string, FdsnArray> arrs;
-    const std::string err = fdsn_read(path, "BK", params_digest, arrs);
-    if (!err.empty()) return set_err(FDSNN_ERR_PARAMETER, "%s: %s", path, err.c_str());
-    const DevParams& d = ctx->dp;
-    auto shape_is = [&](const char* name, std::vector<int64_t> want) {
-        auto it = arrs.find(name);
-        return it != arrs.end() && it->second.shape == want;
-    };
-    const int64_t kr = (int64_t)d.N * d.ks_L;
-    if (!shape_is("ek_a", {d.n, 2 * d.L, d.N}) || !shape_is("ek_b", {d.n, 2 * d.L, d.N}) ||
-        !shape_is("ksk_A", {kr, d.n}) || !shape_is("ksk_b", {kr}))
-        return set_err(FDSNN_ERR_PARAMETER, "%s: key arrays do not match the parameters", path);
-    // rows (n, 2l, 2, N): [i][row][a|b][coef]
-    const auto& ea = arrs["ek_a"].data;
-    const auto& eb = arrs["ek_b"].data;
-    std::vector<int64_t> rows((size_t)d.n * 2 * d.L * 2 * d.N);
-    const size_t poly = (size_t)d.N;
-    for (size_t r = 0; r < (size_t)d.n * 2 * d.L; ++r) {
-        std::memcpy(&rows[(2 * r) * poly], &ea[r * poly], poly * 8);
-        std::memcpy(&rows[(2 * r + 1) * poly], &eb[r * poly], poly * 8);
-    }
-    return fdsnn_bsk_load(ctx, rows.data(), arrs["ksk_A"].data.data(), arrs["ksk_b"].data.data());
+    return guarded([&]() -> int {
+        if (!ctx || !path) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        std::map<std::string, FdsnArray> arrs;
+        const std::string err = fdsn_read(path, "BK", params_digest, arrs);
+        if (!err.empty()) return set_err(FDSNN_ERR_PARAMETER, "%s: %s", path, err.c_str());
+        const DevParams& d = ctx->dp;
+        auto shape_is = [&](const char* name, std::vector<int64_t> want) {
+            auto it = arrs.find(name);
+            return it != arrs.end() && it->second.shape == want;
+        };
+        const int64_t kr = (int64_t)d.N * d.ks_L;
+        if (!shape_is("ek_a", {d.n, 2 * d.L, d.N}) || !shape_is("ek_b", {d.n, 2 * d.L, d.N}) ||
+            !shape_is("ksk_A", {kr, d.n}) || !shape_is("ksk_b", {kr}))
+            return set_err(FDSNN_ERR_PARAMETER, "%s: key arrays do not match the parameters", path);
+        // rows (n, 2l, 2, N): [i][row][a|b][coef]
+        const auto& ea = arrs["ek_a"].data;
+        const auto& eb = arrs["ek_b"].data;
+        std::vector<int64_t> rows((size_t)d.n * 2 * d.L * 2 * d.N);
+        const size_t poly = (size_t)d.N;
+        for (size_t r = 0; r < (size_t)d.n * 2 * d.L; ++r) {
+            std::memcpy(&rows[(2 * r) * poly], &ea[r * poly], poly * 8);
+            std::memcpy(&rows[(2 * r + 1) * poly], &eb[r * poly], poly * 8);
+        }
+        return fdsnn_bsk_load(ctx, rows.data(), arrs["ksk_A"].data.data(), arrs["ksk_b"].data.data());
+    });
 }
 
 int fdsnn_ciphertexts_load_fdsn(fdsnn_ctx* ctx, const char* path, const char* params_digest,
                                 int64_t* count, int32_t* ndim, int64_t* shape, uint32_t* d_rows,
                                 void* stream) {
-    if (!ctx || !path || !count) return set_err(FDSNN_ERR_PARAMETER, "null argument");
-    std::map<std::string, FdsnArray> arrs;
-    const std::string err = fdsn_read(path, "CT", params_digest, arrs);
-    if (!err.empty()) return set_err(FDSNN_ERR_PARAMETER, "%s: %s", path, err.c_str());
-    if (!arrs.count("A") || !arrs.count("b") || !arrs.count("shape"))
-        return set_err(FDSNN_ERR_PARAMETER, "%s: missing arrays", path);
-    const FdsnArray& A = arrs["A"];
-    const FdsnArray& b = arrs["b"];
-    const int64_t cnt = b.shape.empty() ? 0 : b.shape[0];
-    if (A.shape.size() != 2 || A.shape[0] != cnt || A.shape[1] != ctx->dp.n)
-        return set_err(FDSNN_ERR_PARAMETER, "%s: mask array does not match n=%d", path, ctx->dp.n);
-    *count = cnt;
-    const FdsnArray& sh = arrs["shape"];
-    if (ndim) *ndim = (int32_t)sh.data.size();
-    if (shape) for (size_t i = 0; i < sh.data.size() && i < 8; ++i) shape[i] = sh.data[i];
-    if (!d_rows) return FDSNN_OK;
-    return fdsnn_rows_from_host(ctx, A.data.data(), b.data.data(), cnt, d_rows, stream);
+    return guarded([&]() -> int {
+        if (!ctx || !path || !count) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        std::map<std::string, FdsnArray> arrs;
+        const std::string err = fdsn_read(path, "CT", params_digest, arrs);
+        if (!err.empty()) return set_err(FDSNN_ERR_PARAMETER, "%s: %s", path, err.c_str());
+        if (!arrs.count("A") || !arrs.count("b") || !arrs.count("shape"))
+            return set_err(FDSNN_ERR_PARAMETER, "%s: missing arrays", path);
+        const FdsnArray& A = arrs["A"];
+        const FdsnArray& b = arrs["b"];
+        if (b.shape.size() != 1) return set_err(FDSNN_ERR_PARAMETER, "%s: body array must be 1-D", path);
+        const int64_t cnt = b.shape[0];
+        if (A.shape.size() != 2 || A.shape[0] != cnt || A.shape[1] != ctx->dp.n)
+            return set_err(FDSNN_ERR_PARAMETER, "%s: mask array does not match n=%d", path, ctx->dp.n);
+        if ((int64_t)b.data.size() != cnt || (int64_t)A.data.size() != cnt * ctx->dp.n)
+            return set_err(FDSNN_ERR_PARAMETER, "%s: array payloads do not match their shapes", path);
+        *count = cnt;
+        const FdsnArray& sh = arrs["shape"];
+        if (ndim) *ndim = (int32_t)sh.data.size();
+        if (shape) for (size_t i = 0; i < sh.data.size() && i < 8; ++i) shape[i] = sh.data[i];
+        if (!d_rows) return FDSNN_OK;
+        return fdsnn_rows_from_host(ctx, A.data.data(), b.data.data(), cnt, d_rows, stream);
+    });
 }
 
 int fdsnn_lut_load(fdsnn_ctx* ctx, const int64_t* testpoly, int32_t* lut_id) {
-    if (!ctx || !testpoly || !lut_id) return set_err(FDSNN_ERR_PARAMETER, "null argument");
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    CU(cudaSetDevice(ctx->device));
-    std::vector<int32_t> h(ctx->dp.N);
-    for (int j = 0; j < ctx->dp.N; ++j) h[j] = (int32_t)((uint32_t)testpoly[j] & ctx->dp.qmask);
-    int32_t* d = nullptr;
-    CU(cudaMalloc(&d, h.size() * 4));
-    CU(cudaMemcpy(d, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
-    ctx->luts.push_back(d);
-    *lut_id = (int32_t)ctx->luts.size() - 1;
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx || !testpoly || !lut_id) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        std::vector<int32_t> h(ctx->dp.N);
+        for (int j = 0; j < ctx->dp.N; ++j) h[j] = (int32_t)((uint32_t)testpoly[j] & ctx->dp.qmask);
+        int32_t* d = nullptr;
+        CU(cudaMalloc(&d, h.size() * 4));
+        CU(cudaMemcpy(d, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+        ctx->luts.push_back(d);
+        *lut_id = (int32_t)ctx->luts.size() - 1;
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_rows_from_host(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b, int64_t count,
                          uint32_t* d_rows, void* stream) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    if (count <= 0) return FDSNN_OK;
-    cudaStream_t s = pick(ctx, stream);
-    const DevParams& d = ctx->dp;
-    const size_t abytes = (size_t)count * d.n * 8, bbytes = (size_t)count * 8;
-    int rc;
-    if ((rc = ctx->host_stage.ensure(abytes + bbytes))) return rc;
-    int64_t* dA = (int64_t*)ctx->host_stage.p;
-    int64_t* db = dA + (size_t)count * d.n;
-    CU(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(db, b, bbytes, cudaMemcpyHostToDevice, s));
-    rows_pack_kernel<<<grid1d(count * d.stride), 256, 0, s>>>(dA, db, count, d.n, d.stride, d.qmask, d_rows);
-    CU(cudaGetLastError());
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        return rows_from_host_impl(ctx, A, b, count, d_rows, pick(ctx, stream));
+    });
 }
 
 // Stage the binary secret key s (n values) as int32 on the device.
@@ -670,249 +744,261 @@ int stage_secret(fdsnn_ctx* ctx, const int64_t* s, int32_t* dst, cudaStream_t st
         if (s[i] != 0 && s[i] != 1) return set_err(FDSNN_ERR_DOMAIN, "secret key entries must be 0/1");
         h[i] = (int32_t)s[i];
     }
+    // pageable source: staged by the runtime before the call returns
     CU(cudaMemcpyAsync(dst, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st));
     return FDSNN_OK;
 }
 
 int fdsnn_encrypt_rows(fdsnn_ctx* ctx, const int64_t* sk, const int64_t* A, const int64_t* e,
                        const int64_t* m, int64_t count, uint32_t* d_rows, void* stream) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    if (count < 0) return set_err(FDSNN_ERR_PARAMETER, "negative count");
-    if (count == 0) return FDSNN_OK;
-    if (!sk || !A || !e || !m || !d_rows) return set_err(FDSNN_ERR_PARAMETER, "null argument");
-    const DevParams& d = ctx->dp;
-    for (int64_t i = 0; i < count; ++i)
-        if (m[i] < -d.p / 2 + 1 || m[i] > d.p / 2) return set_err(FDSNN_ERR_DOMAIN, "message outside centered Z_p");
-    CU(cudaSetDevice(ctx->device));
-    cudaStream_t st = pick(ctx, stream);
-    const size_t abytes = (size_t)count * d.n * 8, bbytes = (size_t)count * 8;
-    int rc;
-    if ((rc = ctx->host_stage.ensure(abytes + 2 * bbytes + (size_t)d.n * 4 + 16))) return rc;
-    int64_t* dA = (int64_t*)ctx->host_stage.p;
-    int64_t* de = dA + (size_t)count * d.n;
-    int64_t* dm = de + count;
-    int32_t* ds = reinterpret_cast<int32_t*>(dm + count);
-    CU(cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(de, e, bbytes, cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(dm, m, bbytes, cudaMemcpyHostToDevice, st));
-    if ((rc = stage_secret(ctx, sk, ds, st))) return rc;
-    rows_pack_kernel<<<grid1d(count * d.stride), 256, 0, st>>>(dA, de, count, d.n, d.stride, d.qmask, d_rows);
-    CU(cudaGetLastError());
-    const uint32_t delta = (uint32_t)((1ll << d.log2q) / d.p);
-    lwe_encrypt_kernel<<<(unsigned)((count * 32 + 255) / 256), 256, 0, st>>>(d_rows, count, d.stride, d.n, ds, de,
-                                                                           dm, d.qmask, delta);
-    CU(cudaGetLastError());
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        if (count < 0) return set_err(FDSNN_ERR_PARAMETER, "negative count");
+        if (count == 0) return FDSNN_OK;
+        if (!sk || !A || !e || !m || !d_rows) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        const DevParams& d = ctx->dp;
+        for (int64_t i = 0; i < count; ++i)
+            if (m[i] < -d.p / 2 + 1 || m[i] > d.p / 2) return set_err(FDSNN_ERR_DOMAIN, "message outside centered Z_p");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        cudaStream_t st = pick(ctx, stream);
+        const size_t bbytes = (size_t)count * 8;
+        int rc;
+        Buf& stage = ctx->scratch[st].stage;
+        // the stage is stream-ordered: its previous readers on st precede these copies
+        if ((rc = stage.ensure(2 * bbytes + (size_t)d.n * 4 + 16))) return rc;
+        int64_t* de = (int64_t*)stage.p;
+        int64_t* dm = de + count;
+        int32_t* ds = reinterpret_cast<int32_t*>(dm + count);
+        CU(cudaMemcpyAsync(de, e, bbytes, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(dm, m, bbytes, cudaMemcpyHostToDevice, st));
+        if ((rc = stage_secret(ctx, sk, ds, st))) return rc;
+        // masks packed on the host (the body column is overwritten below)
+        if ((rc = rows_from_host_impl(ctx, A, e, count, d_rows, st))) return rc;
+        const uint32_t delta = (uint32_t)((1ll << d.log2q) / d.p);
+        lwe_encrypt_kernel<<<(unsigned)((count * 32 + 255) / 256), 256, 0, st>>>(d_rows, count, d.stride, d.n, ds, de,
+                                                                               dm, d.qmask, delta);
+        CU(cudaGetLastError());
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_decrypt_rows(fdsnn_ctx* ctx, const int64_t* sk, const uint32_t* d_rows, int64_t count, int64_t* m,
                        void* stream) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    if (count < 0) return set_err(FDSNN_ERR_PARAMETER, "negative count");
-    if (count == 0) return FDSNN_OK;
-    if (!sk || !d_rows || !m) return set_err(FDSNN_ERR_PARAMETER, "null argument");
-    const DevParams& d = ctx->dp;
-    CU(cudaSetDevice(ctx->device));
-    cudaStream_t st = pick(ctx, stream);
-    int rc;
-    if ((rc = ctx->host_stage.ensure((size_t)count * 8 + (size_t)d.n * 4 + 16))) return rc;
-    int64_t* dout = (int64_t*)ctx->host_stage.p;
-    int32_t* ds = reinterpret_cast<int32_t*>(dout + count);
-    if ((rc = stage_secret(ctx, sk, ds, st))) return rc;
-    lwe_decrypt_kernel<<<(unsigned)((count * 32 + 255) / 256), 256, 0, st>>>(d_rows, count, d.stride, d.n, ds,
-                                                                           d.log2q, d.p, dout);
-    CU(cudaGetLastError());
-    CU(cudaMemcpyAsync(m, dout, (size_t)count * 8, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        if (count < 0) return set_err(FDSNN_ERR_PARAMETER, "negative count");
+        if (count == 0) return FDSNN_OK;
+        if (!sk || !d_rows || !m) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        const DevParams& d = ctx->dp;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        cudaStream_t st = pick(ctx, stream);
+        int rc;
+        Buf& stage = ctx->scratch[st].stage;
+        if ((rc = stage.ensure((size_t)count * 8 + (size_t)d.n * 4 + 16))) return rc;
+        int64_t* dout = (int64_t*)stage.p;
+        int32_t* ds = reinterpret_cast<int32_t*>(dout + count);
+        if ((rc = stage_secret(ctx, sk, ds, st))) return rc;
+        lwe_decrypt_kernel<<<(unsigned)((count * 32 + 255) / 256), 256, 0, st>>>(d_rows, count, d.stride, d.n, ds,
+                                                                               d.log2q, d.p, dout);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(m, dout, (size_t)count * 8, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_rows_to_host(fdsnn_ctx* ctx, const uint32_t* d_rows, int64_t count, int64_t* A,
                        int64_t* b, void* stream) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    if (count <= 0) return FDSNN_OK;
-    cudaStream_t s = pick(ctx, stream);
-    const DevParams& d = ctx->dp;
-    const size_t abytes = (size_t)count * d.n * 8, bbytes = (size_t)count * 8;
-    int rc;
-    if ((rc = ctx->host_stage.ensure(abytes + bbytes))) return rc;
-    int64_t* dA = (int64_t*)ctx->host_stage.p;
-    int64_t* db = dA + (size_t)count * d.n;
-    rows_unpack_kernel<<<grid1d(count * (d.n + 1)), 256, 0, s>>>(d_rows, count, d.n, d.stride, dA, db);
-    CU(cudaGetLastError());
-    CU(cudaMemcpyAsync(A, dA, abytes, cudaMemcpyDeviceToHost, s));
-    CU(cudaMemcpyAsync(b, db, bbytes, cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        return rows_to_host_impl(ctx, d_rows, count, A, b, pick(ctx, stream));
+    });
 }
 
 int fdsnn_pbs_dev(fdsnn_ctx* ctx, int32_t nlut, const int32_t* lut_ids, const int64_t* in_boff,
                   const int64_t* out_boff, const uint32_t* d_in, const uint32_t* d_in2,
                   int64_t count, uint32_t* d_out, void* stream) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    CU(cudaSetDevice(ctx->device));
-    return pbs_pipeline(ctx, nlut, lut_ids, in_boff, out_boff, d_in, d_in2, count, d_out, pick(ctx, stream));
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        return pbs_pipeline(ctx, nlut, lut_ids, in_boff, out_boff, d_in, d_in2, count, d_out, pick(ctx, stream));
+    });
 }
 
 int fdsnn_pbs_batch(fdsnn_ctx* ctx, int32_t lut_id, const int64_t* A, const int64_t* b,
                     int64_t count, int64_t* outA, int64_t* outb) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    CU(cudaSetDevice(ctx->device));
-    if (count <= 0) return FDSNN_OK;
-    int rc;
-    const size_t rb = (size_t)count * ctx->dp.stride * 4;
-    if ((rc = ctx->rows_a.ensure(rb)) || (rc = ctx->rows_b.ensure(rb))) return rc;
-    if ((rc = fdsnn_rows_from_host(ctx, A, b, count, (uint32_t*)ctx->rows_a.p, ctx->stream))) return rc;
-    if ((rc = pbs_pipeline(ctx, 1, &lut_id, nullptr, nullptr, (uint32_t*)ctx->rows_a.p, nullptr,
-                           count, (uint32_t*)ctx->rows_b.p, ctx->stream)))
-        return rc;
-    return fdsnn_rows_to_host(ctx, (uint32_t*)ctx->rows_b.p, count, outA, outb, ctx->stream);
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        if (count <= 0) return FDSNN_OK;
+        int rc;
+        const size_t rb = (size_t)count * ctx->dp.stride * 4;
+        if ((rc = ctx->rows_a.ensure(rb)) || (rc = ctx->rows_b.ensure(rb))) return rc;
+        if ((rc = rows_from_host_impl(ctx, A, b, count, (uint32_t*)ctx->rows_a.p, ctx->stream))) return rc;
+        if ((rc = pbs_pipeline(ctx, 1, &lut_id, nullptr, nullptr, (uint32_t*)ctx->rows_a.p, nullptr,
+                               count, (uint32_t*)ctx->rows_b.p, ctx->stream)))
+            return rc;
+        return rows_to_host_impl(ctx, (uint32_t*)ctx->rows_b.p, count, outA, outb, ctx->stream);
+    });
 }
 
 int fdsnn_lif_step_batch(fdsnn_ctx* ctx, int32_t lut_fire, int32_t lut_reset, int64_t v_th_hat,
                          const int64_t* vA, const int64_t* vb, const int64_t* iA, const int64_t* ib,
                          int64_t count, int64_t* sA, int64_t* sb, int64_t* nA, int64_t* nb) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    CU(cudaSetDevice(ctx->device));
-    if (count <= 0) return FDSNN_OK;
-    int rc;
-    const size_t rb = (size_t)count * ctx->dp.stride * 4;
-    if ((rc = ctx->rows_a.ensure(rb)) || (rc = ctx->rows_b.ensure(rb)) ||
-        (rc = ctx->rows_c.ensure(2 * rb)))
-        return rc;
-    uint32_t* rv = (uint32_t*)ctx->rows_a.p;
-    uint32_t* ri = (uint32_t*)ctx->rows_b.p;
-    uint32_t* ro = (uint32_t*)ctx->rows_c.p;
-    if ((rc = fdsnn_rows_from_host(ctx, vA, vb, count, rv, ctx->stream))) return rc;
-    // rows_from_host reuses the staging buffer: order the two uploads on the stream
-    if ((rc = fdsnn_rows_from_host(ctx, iA, ib, count, ri, ctx->stream))) return rc;
-    const int32_t luts[2] = {lut_fire, lut_reset};
-    const int64_t inb[2] = {-v_th_hat, 0};
-    const int64_t outb[2] = {1, 0};
-    if ((rc = pbs_pipeline(ctx, 2, luts, inb, outb, rv, ri, count, ro, ctx->stream))) return rc;
-    if ((rc = fdsnn_rows_to_host(ctx, ro, count, sA, sb, ctx->stream))) return rc;
-    return fdsnn_rows_to_host(ctx, ro + (size_t)count * ctx->dp.stride, count, nA, nb, ctx->stream);
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        if (count <= 0) return FDSNN_OK;
+        int rc;
+        const size_t rb = (size_t)count * ctx->dp.stride * 4;
+        if ((rc = ctx->rows_a.ensure(rb)) || (rc = ctx->rows_b.ensure(rb)) ||
+            (rc = ctx->rows_c.ensure(2 * rb)))
+            return rc;
+        uint32_t* rv = (uint32_t*)ctx->rows_a.p;
+        uint32_t* ri = (uint32_t*)ctx->rows_b.p;
+        uint32_t* ro = (uint32_t*)ctx->rows_c.p;
+        if ((rc = rows_from_host_impl(ctx, vA, vb, count, rv, ctx->stream))) return rc;
+        if ((rc = rows_from_host_impl(ctx, iA, ib, count, ri, ctx->stream))) return rc;
+        const int32_t luts[2] = {lut_fire, lut_reset};
+        const int64_t inb[2] = {-v_th_hat, 0};
+        const int64_t outb[2] = {1, 0};
+        if ((rc = pbs_pipeline(ctx, 2, luts, inb, outb, rv, ri, count, ro, ctx->stream))) return rc;
+        if ((rc = rows_to_host_impl(ctx, ro, count, sA, sb, ctx->stream))) return rc;
+        return rows_to_host_impl(ctx, ro + (size_t)count * ctx->dp.stride, count, nA, nb, ctx->stream);
+    });
 }
 
 int fdsnn_blind_rotate_batch(fdsnn_ctx* ctx, int64_t* acc, const int64_t* a2N, int64_t count) {
-    int rc;
-    if ((rc = check_keys(ctx))) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    CU(cudaSetDevice(ctx->device));
-    if (count <= 0) return FDSNN_OK;
-    const DevParams& d = ctx->dp;
-    const size_t accn = (size_t)count * 2 * d.N, kn = (size_t)count * d.n;
-    std::vector<int32_t> h_acc(accn), h_k(kn);
-    for (size_t i = 0; i < accn; ++i) h_acc[i] = (int32_t)((uint32_t)acc[i] & d.qmask);
-    for (size_t i = 0; i < kn; ++i) h_k[i] = (int32_t)(((a2N[i] % (2 * d.N)) + 2 * d.N) % (2 * d.N));
-    if ((rc = ctx->acc_buf.ensure(accn * 4)) || (rc = ctx->a2n_buf.ensure(kn * 4))) return rc;
-    CU(cudaMemcpyAsync(ctx->acc_buf.p, h_acc.data(), accn * 4, cudaMemcpyHostToDevice, ctx->stream));
-    CU(cudaMemcpyAsync(ctx->a2n_buf.p, h_k.data(), kn * 4, cudaMemcpyHostToDevice, ctx->stream));
-    PbsArgs a{};
-    a.prm = d;
-    a.count = count;
-    a.nlut = 1;
-    a.acc_io = (int32_t*)ctx->acc_buf.p;
-    a.a2N_in = (const int32_t*)ctx->a2n_buf.p;
-    a.bsk = ctx->bsk;
-    a.tables = ctx->tables;
-    a.margin = ctx->margin;
-    if ((rc = launch_br(ctx, a, count, true, ctx->stream))) return rc;
-    CU(cudaMemcpyAsync(h_acc.data(), ctx->acc_buf.p, accn * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
-    for (size_t i = 0; i < accn; ++i) acc[i] = (int64_t)(uint32_t)h_acc[i];
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        int rc;
+        if ((rc = check_keys(ctx))) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        if (count <= 0) return FDSNN_OK;
+        const DevParams& d = ctx->dp;
+        const size_t accn = (size_t)count * 2 * d.N, kn = (size_t)count * d.n;
+        std::vector<int32_t> h_acc(accn), h_k(kn);
+        for (size_t i = 0; i < accn; ++i) h_acc[i] = (int32_t)((uint32_t)acc[i] & d.qmask);
+        for (size_t i = 0; i < kn; ++i) h_k[i] = (int32_t)(((a2N[i] % (2 * d.N)) + 2 * d.N) % (2 * d.N));
+        if ((rc = ctx->acc_buf.ensure(accn * 4)) || (rc = ctx->a2n_buf.ensure(kn * 4))) return rc;
+        CU(cudaMemcpyAsync(ctx->acc_buf.p, h_acc.data(), accn * 4, cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->a2n_buf.p, h_k.data(), kn * 4, cudaMemcpyHostToDevice, ctx->stream));
+        PbsArgs a{};
+        a.prm = d;
+        a.count = count;
+        a.nlut = 1;
+        a.acc_io = (int32_t*)ctx->acc_buf.p;
+        a.a2N_in = (const int32_t*)ctx->a2n_buf.p;
+        a.bsk = ctx->bsk;
+        a.tables = ctx->tables;
+        a.margin = ctx->margin;
+        if ((rc = launch_br(ctx, a, count, true, ctx->stream))) return rc;
+        CU(cudaMemcpyAsync(h_acc.data(), ctx->acc_buf.p, accn * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        for (size_t i = 0; i < accn; ++i) acc[i] = (int64_t)(uint32_t)h_acc[i];
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_key_switch_batch(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b, int64_t count,
                            int64_t* outA, int64_t* outb) {
-    int rc;
-    if ((rc = check_keys(ctx))) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    CU(cudaSetDevice(ctx->device));
-    if (count <= 0) return FDSNN_OK;
-    const DevParams& d = ctx->dp;
-    std::vector<uint32_t> h((size_t)count * d.ext_stride, 0u);
-    for (int64_t r = 0; r < count; ++r) {
-        for (int j = 0; j < d.N; ++j) h[r * d.ext_stride + j] = (uint32_t)A[r * d.N + j] & d.qmask;
-        h[r * d.ext_stride + d.N] = (uint32_t)b[r] & d.qmask;
-    }
-    const size_t rb = (size_t)count * d.stride * 4;
-    if ((rc = ctx->ext.ensure(h.size() * 4)) || (rc = ctx->rows_b.ensure(rb))) return rc;
-    CU(cudaMemcpyAsync(ctx->ext.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-    KsArgs k{};
-    k.prm = d;
-    k.ext = (const uint32_t*)ctx->ext.p;
-    k.V = count;
-    k.ksk = ctx->ksk;
-    k.kskb = ctx->kskb;
-    k.out = (uint32_t*)ctx->rows_b.p;
-    k.count = count;
-    if ((rc = launch_ks(ctx, k, ctx->stream))) return rc;
-    return fdsnn_rows_to_host(ctx, (uint32_t*)ctx->rows_b.p, count, outA, outb, ctx->stream);
+    return guarded([&]() -> int {
+        int rc;
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        if (!ctx->ks_loaded) return set_err(FDSNN_ERR_STATE, "key-switch key not loaded");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        if (count <= 0) return FDSNN_OK;
+        const DevParams& d = ctx->dp;
+        std::vector<uint32_t> h((size_t)count * d.ext_stride, 0u);
+        for (int64_t r = 0; r < count; ++r) {
+            for (int j = 0; j < d.N; ++j) h[r * d.ext_stride + j] = (uint32_t)A[r * d.N + j] & d.qmask;
+            h[r * d.ext_stride + d.N] = (uint32_t)b[r] & d.qmask;
+        }
+        const size_t rb = (size_t)count * d.stride * 4;
+        if ((rc = ctx->ext.ensure(h.size() * 4)) || (rc = ctx->rows_b.ensure(rb))) return rc;
+        CU(cudaMemcpyAsync(ctx->ext.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        KsArgs k{};
+        k.prm = d;
+        k.ext = (const uint32_t*)ctx->ext.p;
+        k.V = count;
+        k.ksk = ctx->ksk;
+        k.kskb = ctx->kskb;
+        k.out = (uint32_t*)ctx->rows_b.p;
+        k.count = count;
+        if ((rc = launch_ks(ctx, k, ctx->stream))) return rc;
+        return rows_to_host_impl(ctx, (uint32_t*)ctx->rows_b.p, count, outA, outb, ctx->stream);
+    });
 }
 
 int fdsnn_operator_load(fdsnn_ctx* ctx, const int64_t* Mh, int64_t out_cells, int64_t in_cells,
                         int32_t* op_id) {
-    if (!ctx || !Mh || !op_id) return set_err(FDSNN_ERR_PARAMETER, "null argument");
-    if (out_cells <= 0 || in_cells <= 0 || out_cells > (1 << 30) || in_cells > (1 << 30))
-        return set_err(FDSNN_ERR_PARAMETER, "bad operator shape");
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    CU(cudaSetDevice(ctx->device));
-    Operator op;
-    op.out_cells = (int)out_cells;
-    op.in_cells = (int)in_cells;
-    int64_t nnz = 0;
-    const int64_t total = out_cells * in_cells;
-    for (int64_t i = 0; i < total; ++i) {
-        if (Mh[i] > INT32_MAX || Mh[i] < INT32_MIN)
-            return set_err(FDSNN_ERR_PARAMETER, "operator weight out of int32 range");
-        nnz += Mh[i] != 0;
-    }
-    op.dense = nnz * 4 > total;
-    if (op.dense) {
-        std::vector<int32_t> w((size_t)total);
-        for (int64_t i = 0; i < total; ++i) w[i] = (int32_t)Mh[i];
-        CU(cudaMalloc(&op.w, w.size() * 4));
-        CU(cudaMemcpy(op.w, w.data(), w.size() * 4, cudaMemcpyHostToDevice));
-    } else {
-        std::vector<int32_t> rp(out_cells + 1), ci, va;
-        ci.reserve(nnz);
-        va.reserve(nnz);
-        for (int64_t r = 0; r < out_cells; ++r) {
-            rp[r] = (int32_t)ci.size();
-            for (int64_t c = 0; c < in_cells; ++c) {
-                const int64_t x = Mh[r * in_cells + c];
-                if (x) { ci.push_back((int32_t)c); va.push_back((int32_t)x); }
+    return guarded([&]() -> int {
+        if (!ctx || !Mh || !op_id) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        if (out_cells <= 0 || in_cells <= 0 || out_cells > (1 << 30) || in_cells > (1 << 30))
+            return set_err(FDSNN_ERR_PARAMETER, "bad operator shape");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        Operator op;
+        op.out_cells = (int)out_cells;
+        op.in_cells = (int)in_cells;
+        int64_t nnz = 0;
+        const int64_t total = out_cells * in_cells;
+        for (int64_t i = 0; i < total; ++i) {
+            if (Mh[i] > INT32_MAX || Mh[i] < INT32_MIN)
+                return set_err(FDSNN_ERR_PARAMETER, "operator weight out of int32 range");
+            nnz += Mh[i] != 0;
+        }
+        op.dense = nnz * 4 > total;
+        if (op.dense) {
+            std::vector<int32_t> w((size_t)total);
+            for (int64_t i = 0; i < total; ++i) w[i] = (int32_t)Mh[i];
+            CU(cudaMalloc(&op.w, w.size() * 4));
+            CU(cudaMemcpy(op.w, w.data(), w.size() * 4, cudaMemcpyHostToDevice));
+        } else {
+            std::vector<int32_t> rp(out_cells + 1), ci, va;
+            ci.reserve(nnz);
+            va.reserve(nnz);
+            for (int64_t r = 0; r < out_cells; ++r) {
+                rp[r] = (int32_t)ci.size();
+                for (int64_t c = 0; c < in_cells; ++c) {
+                    const int64_t x = Mh[r * in_cells + c];
+                    if (x) { ci.push_back((int32_t)c); va.push_back((int32_t)x); }
+                }
+            }
+            rp[out_cells] = (int32_t)ci.size();
+            CU(cudaMalloc(&op.row_ptr, rp.size() * 4));
+            CU(cudaMemcpy(op.row_ptr, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice));
+            const size_t nb = std::max<size_t>(1, ci.size()) * 4;
+            CU(cudaMalloc(&op.col_idx, nb));
+            CU(cudaMalloc(&op.val, nb));
+            if (!ci.empty()) {
+                CU(cudaMemcpy(op.col_idx, ci.data(), ci.size() * 4, cudaMemcpyHostToDevice));
+                CU(cudaMemcpy(op.val, va.data(), va.size() * 4, cudaMemcpyHostToDevice));
             }
         }
-        rp[out_cells] = (int32_t)ci.size();
-        CU(cudaMalloc(&op.row_ptr, rp.size() * 4));
-        CU(cudaMemcpy(op.row_ptr, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice));
-        const size_t nb = std::max<size_t>(1, ci.size()) * 4;
-        CU(cudaMalloc(&op.col_idx, nb));
-        CU(cudaMalloc(&op.val, nb));
-        if (!ci.empty()) {
-            CU(cudaMemcpy(op.col_idx, ci.data(), ci.size() * 4, cudaMemcpyHostToDevice));
-            CU(cudaMemcpy(op.val, va.data(), va.size() * 4, cudaMemcpyHostToDevice));
-        }
-    }
-    ctx->ops.push_back(op);
-    *op_id = (int32_t)ctx->ops.size() - 1;
-    return FDSNN_OK;
+        ctx->ops.push_back(op);
+        *op_id = (int32_t)ctx->ops.size() - 1;
+        return FDSNN_OK;
+    });
 }
 
-int fdsnn_operator_apply(fdsnn_ctx* ctx, int32_t op_id, const uint32_t* d_in, int64_t batch,
-                         uint32_t* d_out, void* stream) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+}  // extern "C"
+
+namespace {
+// callers hold ctx->mu (ctx->ops may grow concurrently, the timer list is shared)
+int operator_apply_impl(fdsnn_ctx* ctx, int32_t op_id, const uint32_t* d_in, int64_t batch, uint32_t* d_out,
+                        cudaStream_t s) {
     if (op_id < 0 || op_id >= (int32_t)ctx->ops.size()) return set_err(FDSNN_ERR_STATE, "unknown operator %d", op_id);
     if (batch <= 0) return FDSNN_OK;
     if (batch > 65535) return set_err(FDSNN_ERR_PARAMETER, "batch too large");
-    CU(cudaSetDevice(ctx->device));
-    cudaStream_t s = pick(ctx, stream);
     const Operator& op = ctx->ops[op_id];
     const DevParams& d = ctx->dp;
     TimerScope ts(ctx, 2, s);
@@ -932,181 +1018,222 @@ int fdsnn_operator_apply(fdsnn_ctx* ctx, int32_t op_id, const uint32_t* d_in, in
     CU(cudaGetLastError());
     return FDSNN_OK;
 }
+}  // namespace
+
+extern "C" {
+
+int fdsnn_operator_apply(fdsnn_ctx* ctx, int32_t op_id, const uint32_t* d_in, int64_t batch,
+                         uint32_t* d_out, void* stream) {
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        return operator_apply_impl(ctx, op_id, d_in, batch, d_out, pick(ctx, stream));
+    });
+}
 
 int fdsnn_plain_apply(fdsnn_ctx* ctx, int32_t op_id, const int64_t* d_x, int64_t batch, int64_t* d_y,
                       void* stream) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    if (op_id < 0 || op_id >= (int32_t)ctx->ops.size()) return set_err(FDSNN_ERR_STATE, "unknown operator %d", op_id);
-    if (batch < 0) return set_err(FDSNN_ERR_PARAMETER, "negative batch");
-    if (batch == 0) return FDSNN_OK;
-    if (!d_x || !d_y) return set_err(FDSNN_ERR_PARAMETER, "null buffer");
-    CU(cudaSetDevice(ctx->device));
-    cudaStream_t s = pick(ctx, stream);
-    const Operator& op = ctx->ops[op_id];
-    const int64_t warps = batch * op.out_cells;
-    const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
-    if (op.dense)
-        plain_dense_kernel<<<blocks, 256, 0, s>>>(op.w, op.out_cells, op.in_cells, d_x, batch, d_y);
-    else
-        plain_csr_kernel<<<blocks, 256, 0, s>>>(op.row_ptr, op.col_idx, op.val, op.out_cells, op.in_cells, d_x,
-                                                batch, d_y);
-    CU(cudaGetLastError());
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        if (op_id < 0 || op_id >= (int32_t)ctx->ops.size()) return set_err(FDSNN_ERR_STATE, "unknown operator %d", op_id);
+        if (batch < 0) return set_err(FDSNN_ERR_PARAMETER, "negative batch");
+        if (batch == 0) return FDSNN_OK;
+        if (!d_x || !d_y) return set_err(FDSNN_ERR_PARAMETER, "null buffer");
+        CU(cudaSetDevice(ctx->device));
+        cudaStream_t s = pick(ctx, stream);
+        const Operator& op = ctx->ops[op_id];
+        const int64_t warps = batch * op.out_cells;
+        const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
+        if (op.dense)
+            plain_dense_kernel<<<blocks, 256, 0, s>>>(op.w, op.out_cells, op.in_cells, d_x, batch, d_y);
+        else
+            plain_csr_kernel<<<blocks, 256, 0, s>>>(op.row_ptr, op.col_idx, op.val, op.out_cells, op.in_cells, d_x,
+                                                    batch, d_y);
+        CU(cudaGetLastError());
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_plain_lif(fdsnn_ctx* ctx, const int64_t* d_v, const int64_t* d_i, int64_t count, int64_t v_th_hat,
                     int64_t leak_num, int64_t leak_den, int64_t p, int64_t* d_spike2, int64_t* d_v_next,
                     uint64_t* d_overflow, void* stream) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    if (count < 0 || leak_den <= 0 || p < 0) return set_err(FDSNN_ERR_PARAMETER, "bad LIF arguments");
-    if (count == 0) return FDSNN_OK;
-    if (!d_v || !d_i || !d_spike2 || !d_v_next || (p > 0 && !d_overflow))
-        return set_err(FDSNN_ERR_PARAMETER, "null buffer");
-    CU(cudaSetDevice(ctx->device));
-    cudaStream_t s = pick(ctx, stream);
-    plain_lif_kernel<<<grid1d(count), 256, 0, s>>>(d_v, d_i, count, v_th_hat, leak_num, leak_den, p, d_spike2,
-                                                   d_v_next, reinterpret_cast<unsigned long long*>(d_overflow));
-    CU(cudaGetLastError());
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        if (count < 0 || leak_den <= 0 || p < 0) return set_err(FDSNN_ERR_PARAMETER, "bad LIF arguments");
+        if (count == 0) return FDSNN_OK;
+        if (!d_v || !d_i || !d_spike2 || !d_v_next || (p > 0 && !d_overflow))
+            return set_err(FDSNN_ERR_PARAMETER, "null buffer");
+        CU(cudaSetDevice(ctx->device));
+        cudaStream_t s = pick(ctx, stream);
+        plain_lif_kernel<<<grid1d(count), 256, 0, s>>>(d_v, d_i, count, v_th_hat, leak_num, leak_den, p, d_spike2,
+                                                       d_v_next, reinterpret_cast<unsigned long long*>(d_overflow));
+        CU(cudaGetLastError());
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_weight_sum(fdsnn_ctx* ctx, const int64_t* Mh, int64_t out_cells, int64_t in_cells,
                      const int64_t* A, const int64_t* b, int64_t* outA, int64_t* outb) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    int32_t id;
-    int rc;
-    if ((rc = fdsnn_operator_load(ctx, Mh, out_cells, in_cells, &id))) return rc;
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    const DevParams& d = ctx->dp;
-    if ((rc = ctx->rows_a.ensure((size_t)in_cells * d.stride * 4)) ||
-        (rc = ctx->rows_b.ensure((size_t)out_cells * d.stride * 4)))
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        int32_t id;
+        int rc;
+        if ((rc = fdsnn_operator_load(ctx, Mh, out_cells, in_cells, &id))) return rc;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        const DevParams& d = ctx->dp;
+        if ((rc = ctx->rows_a.ensure((size_t)in_cells * d.stride * 4)) ||
+            (rc = ctx->rows_b.ensure((size_t)out_cells * d.stride * 4)))
+            return rc;
+        if ((rc = rows_from_host_impl(ctx, A, b, in_cells, (uint32_t*)ctx->rows_a.p, ctx->stream))) return rc;
+        if ((rc = operator_apply_impl(ctx, id, (uint32_t*)ctx->rows_a.p, 1, (uint32_t*)ctx->rows_b.p, ctx->stream))) return rc;
+        rc = rows_to_host_impl(ctx, (uint32_t*)ctx->rows_b.p, out_cells, outA, outb, ctx->stream);
+        // one-shot operator: release its device storage
+        Operator& op = ctx->ops[id];
+        cudaFree(op.w); cudaFree(op.row_ptr); cudaFree(op.col_idx); cudaFree(op.val);
+        op = Operator{};
         return rc;
-    if ((rc = fdsnn_rows_from_host(ctx, A, b, in_cells, (uint32_t*)ctx->rows_a.p, ctx->stream))) return rc;
-    if ((rc = fdsnn_operator_apply(ctx, id, (uint32_t*)ctx->rows_a.p, 1, (uint32_t*)ctx->rows_b.p, ctx->stream))) return rc;
-    rc = fdsnn_rows_to_host(ctx, (uint32_t*)ctx->rows_b.p, out_cells, outA, outb, ctx->stream);
-    // one-shot operator: release its device storage
-    Operator& op = ctx->ops[id];
-    cudaFree(op.w); cudaFree(op.row_ptr); cudaFree(op.col_idx); cudaFree(op.val);
-    op = Operator{};
-    return rc;
+    });
 }
 
 int fdsnn_rows_add(fdsnn_ctx* ctx, const uint32_t* d_x, const uint32_t* d_y, int64_t count,
                    uint32_t* d_out, void* stream) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    if (count <= 0) return FDSNN_OK;
-    cudaStream_t s = pick(ctx, stream);
-    const int64_t words = count * ctx->dp.stride;
-    rows_add_kernel<<<grid1d(words), 256, 0, s>>>(d_x, d_y, d_out, words, ctx->dp.qmask);
-    CU(cudaGetLastError());
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        if (count <= 0) return FDSNN_OK;
+        cudaStream_t s = pick(ctx, stream);
+        const int64_t words = count * ctx->dp.stride;
+        rows_add_kernel<<<grid1d(words), 256, 0, s>>>(d_x, d_y, d_out, words, ctx->dp.qmask);
+        CU(cudaGetLastError());
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_dev_alloc(fdsnn_ctx* ctx, int64_t bytes, void** ptr) {
-    if (!ctx || !ptr) return set_err(FDSNN_ERR_PARAMETER, "null argument");
-    CU(cudaSetDevice(ctx->device));
-    CU(cudaMalloc(ptr, (size_t)std::max<int64_t>(bytes, 4)));
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx || !ptr) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        CU(cudaSetDevice(ctx->device));
+        CU(cudaMalloc(ptr, (size_t)std::max<int64_t>(bytes, 4)));
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_dev_free(fdsnn_ctx* ctx, void* ptr) {
-    if (!ctx) return set_err(FDSNN_ERR_PARAMETER, "null argument");
-    CU(cudaFree(ptr));
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        CU(cudaFree(ptr));
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_sync(fdsnn_ctx* ctx) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    CU(cudaStreamSynchronize(ctx->stream));
-    CU(cudaDeviceSynchronize());
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        CU(cudaStreamSynchronize(ctx->stream));
+        CU(cudaDeviceSynchronize());
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_timing_enable(fdsnn_ctx* ctx, int32_t on) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    ctx->timing = on != 0;
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        ctx->timing = on != 0;
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_timing_read(fdsnn_ctx* ctx, int32_t which, double* ms, int64_t* launches) {
-    if (!ctx || which < 0 || which > 2) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
-    for (auto& t : ctx->timed) {
-        CU(cudaEventSynchronize(t.b));
-        float e = 0.f;
-        CU(cudaEventElapsedTime(&e, t.a, t.b));
-        ctx->timed_ms[t.which] += e;
-        ctx->timed_n[t.which] += t.kernels;
-        cudaEventDestroy(t.a);
-        cudaEventDestroy(t.b);
-    }
-    ctx->timed.clear();
-    if (ms) *ms = ctx->timed_ms[which];
-    if (launches) *launches = ctx->timed_n[which];
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx || which < 0 || which > 2) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
+        for (auto& t : ctx->timed) {
+            CU(cudaEventSynchronize(t.b));
+            float e = 0.f;
+            CU(cudaEventElapsedTime(&e, t.a, t.b));
+            ctx->timed_ms[t.which] += e;
+            ctx->timed_n[t.which] += t.kernels;
+            cudaEventDestroy(t.a);
+            cudaEventDestroy(t.b);
+        }
+        ctx->timed.clear();
+        if (ms) *ms = ctx->timed_ms[which];
+        if (launches) *launches = ctx->timed_n[which];
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_timing_reset(fdsnn_ctx* ctx) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    double ms;
-    int64_t n;
-    fdsnn_timing_read(ctx, 0, &ms, &n);
-    for (int i = 0; i < 3; ++i) { ctx->timed_ms[i] = 0; ctx->timed_n[i] = 0; }
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        double ms;
+        int64_t n;
+        fdsnn_timing_read(ctx, 0, &ms, &n);
+        for (int i = 0; i < 3; ++i) { ctx->timed_ms[i] = 0; ctx->timed_n[i] = 0; }
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_margin_enable(fdsnn_ctx* ctx, int32_t on) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    ctx->track_margin = on != 0;
-    CU(cudaMemset(ctx->margin, 0, sizeof(unsigned long long)));
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        ctx->track_margin = on != 0;
+        CU(cudaMemset(ctx->margin, 0, sizeof(unsigned long long)));
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_margin_read(fdsnn_ctx* ctx, double* max_err) {
-    if (!ctx || !max_err) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
-    unsigned long long bits = 0;
-    CU(cudaStreamSynchronize(ctx->stream));
-    CU(cudaMemcpy(&bits, ctx->margin, sizeof bits, cudaMemcpyDeviceToHost));
-    double v;
-    std::memcpy(&v, &bits, sizeof v);
-    *max_err = v;
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx || !max_err) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
+        unsigned long long bits = 0;
+        CU(cudaStreamSynchronize(ctx->stream));
+        CU(cudaMemcpy(&bits, ctx->margin, sizeof bits, cudaMemcpyDeviceToHost));
+        double v;
+        std::memcpy(&v, &bits, sizeof v);
+        *max_err = v;
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_probe_fp64_peak(fdsnn_ctx* ctx, double* tflops) {
-    if (!ctx || !tflops) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
-    CU(cudaSetDevice(ctx->device));
-    double* d = nullptr;
-    CU(cudaMalloc(&d, 8));
-    const int blocks = 148 * 8, threads = 256, iters = 2048;
-    cudaEvent_t a, b;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    fp64_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(d, 64);  // warm-up
-    float best = 1e30f;
-    for (int rep = 0; rep < 5; ++rep) {
-        cudaEventRecord(a, ctx->stream);
-        fp64_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(d, iters);
-        cudaEventRecord(b, ctx->stream);
-        CU(cudaEventSynchronize(b));
-        float ms = 0;
-        cudaEventElapsedTime(&ms, a, b);
-        if (ms < best) best = ms;
-    }
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-    cudaFree(d);
-    const double flops = 2.0 * 16 * 8 * (double)iters * blocks * threads;
-    *tflops = flops / (best * 1e-3) / 1e12;
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx || !tflops) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
+        CU(cudaSetDevice(ctx->device));
+        double* d = nullptr;
+        CU(cudaMalloc(&d, 8));
+        const int blocks = 148 * 8, threads = 256, iters = 2048;
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        fp64_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(d, 64);  // warm-up
+        float best = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            cudaEventRecord(a, ctx->stream);
+            fp64_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(d, iters);
+            cudaEventRecord(b, ctx->stream);
+            CU(cudaEventSynchronize(b));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, a, b);
+            if (ms < best) best = ms;
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaFree(d);
+        const double flops = 2.0 * 16 * 8 * (double)iters * blocks * threads;
+        *tflops = flops / (best * 1e-3) / 1e12;
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_flush_l2(fdsnn_ctx* ctx, void* stream) {
-    if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
-    const size_t bytes = 256ull << 20;  // 2x the 126 MB L2
-    int rc;
-    if ((rc = ctx->l2flush.ensure(bytes))) return rc;
-    CU(cudaMemsetAsync(ctx->l2flush.p, (int)(ctx->timed_n[0] & 0xff), bytes, pick(ctx, stream)));
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        const size_t bytes = 256ull << 20;  // 2x the 126 MB L2
+        int rc;
+        if ((rc = ctx->l2flush.ensure(bytes))) return rc;
+        CU(cudaMemsetAsync(ctx->l2flush.p, (int)(ctx->timed_n[0] & 0xff), bytes, pick(ctx, stream)));
+        return FDSNN_OK;
+    });
 }
 
 }  // extern "C"
@@ -1157,60 +1284,68 @@ int nt_run(int32_t device, int32_t N, const double* in, double* out, int64_t cou
 extern "C" {
 
 int fdsnn_nt_forward(int32_t device, int32_t N, const double* coeffs, double* evals, int64_t count) {
-    return nt_run<false>(device, N, coeffs, evals, count);
+    return guarded([&]() -> int {
+        return nt_run<false>(device, N, coeffs, evals, count);
+    });
 }
 
 int fdsnn_nt_inverse(int32_t device, int32_t N, const double* evals, double* coeffs, int64_t count) {
-    return nt_run<true>(device, N, evals, coeffs, count);
+    return guarded([&]() -> int {
+        return nt_run<true>(device, N, evals, coeffs, count);
+    });
 }
 
 int fdsnn_negacyclic_mac(int32_t device, int32_t N, int32_t log2_q, int32_t D, const int64_t* x,
                          const int64_t* y, int64_t* out, int64_t count) {
-    if (!is_pow2(N) || N > 4096) return set_err(FDSNN_ERR_PARAMETER, "negacyclic product: N=%d unsupported", N);
-    if (log2_q < 1 || log2_q > 63) return set_err(FDSNN_ERR_PARAMETER, "q must be 2^1..2^63");
-    if (D < 1 || count < 0 || (count > 0 && (!x || !y || !out))) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
-    if (count == 0) return FDSNN_OK;
-    if (int rc = ring_device(device)) return rc;
-    const size_t in_bytes = (size_t)count * D * N * sizeof(int64_t), out_bytes = (size_t)count * N * sizeof(int64_t);
-    DevScratch dx, dy, dout;
-    CU(cudaMalloc(&dx.p, in_bytes));
-    CU(cudaMalloc(&dy.p, in_bytes));
-    CU(cudaMalloc(&dout.p, out_bytes));
-    CU(cudaMemcpy(dx.p, x, in_bytes, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(dy.p, y, in_bytes, cudaMemcpyHostToDevice));
-    const int threads = N < 256 ? (N < 32 ? 32 : N) : 256;
-    const size_t smem = 2 * (size_t)N * sizeof(uint64_t);
-    CU(cudaFuncSetAttribute(negacyclic_mac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const uint64_t qmask = (1ull << log2_q) - 1;
-    for (int64_t b0 = 0; b0 < count; b0 += 65535) {
-        const int64_t nb = count - b0 < 65535 ? count - b0 : 65535;
-        dim3 grid((unsigned)nb, (unsigned)((N + threads - 1) / threads));
-        negacyclic_mac_kernel<<<grid, threads, smem>>>(N, qmask, D, (const int64_t*)dx.p + b0 * D * N,
-                                                      (const int64_t*)dy.p + b0 * D * N,
-                                                      (int64_t*)dout.p + b0 * N);
-        CU(cudaGetLastError());
-    }
-    CU(cudaMemcpy(out, dout.p, out_bytes, cudaMemcpyDeviceToHost));
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (!is_pow2(N) || N > 4096) return set_err(FDSNN_ERR_PARAMETER, "negacyclic product: N=%d unsupported", N);
+        if (log2_q < 1 || log2_q > 63) return set_err(FDSNN_ERR_PARAMETER, "q must be 2^1..2^63");
+        if (D < 1 || count < 0 || (count > 0 && (!x || !y || !out))) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
+        if (count == 0) return FDSNN_OK;
+        if (int rc = ring_device(device)) return rc;
+        const size_t in_bytes = (size_t)count * D * N * sizeof(int64_t), out_bytes = (size_t)count * N * sizeof(int64_t);
+        DevScratch dx, dy, dout;
+        CU(cudaMalloc(&dx.p, in_bytes));
+        CU(cudaMalloc(&dy.p, in_bytes));
+        CU(cudaMalloc(&dout.p, out_bytes));
+        CU(cudaMemcpy(dx.p, x, in_bytes, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(dy.p, y, in_bytes, cudaMemcpyHostToDevice));
+        const int threads = N < 256 ? (N < 32 ? 32 : N) : 256;
+        const size_t smem = 2 * (size_t)N * sizeof(uint64_t);
+        CU(cudaFuncSetAttribute(negacyclic_mac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const uint64_t qmask = (1ull << log2_q) - 1;
+        for (int64_t b0 = 0; b0 < count; b0 += 65535) {
+            const int64_t nb = count - b0 < 65535 ? count - b0 : 65535;
+            dim3 grid((unsigned)nb, (unsigned)((N + threads - 1) / threads));
+            negacyclic_mac_kernel<<<grid, threads, smem>>>(N, qmask, D, (const int64_t*)dx.p + b0 * D * N,
+                                                          (const int64_t*)dy.p + b0 * D * N,
+                                                          (int64_t*)dout.p + b0 * N);
+            CU(cudaGetLastError());
+        }
+        CU(cudaMemcpy(out, dout.p, out_bytes, cudaMemcpyDeviceToHost));
+        return FDSNN_OK;
+    });
 }
 
 int fdsnn_gadget_decompose(int32_t device, int32_t log2_q, int32_t bg_log, int32_t levels, const int64_t* x,
                            int64_t rows, int64_t len, int64_t* digits) {
-    if (log2_q < 1 || log2_q > 62 || bg_log < 1 || levels < 1 || (int64_t)bg_log * levels > 63)
-        return set_err(FDSNN_ERR_PARAMETER, "gadget: q=2^%d, B=2^%d, levels=%d unsupported", log2_q, bg_log, levels);
-    if (rows < 0 || len < 0 || (rows * len > 0 && (!x || !digits))) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
-    if (rows * len == 0) return FDSNN_OK;
-    if (int rc = ring_device(device)) return rc;
-    const size_t in_bytes = (size_t)rows * len * sizeof(int64_t);
-    DevScratch dx, dd;
-    CU(cudaMalloc(&dx.p, in_bytes));
-    CU(cudaMalloc(&dd.p, in_bytes * levels));
-    CU(cudaMemcpy(dx.p, x, in_bytes, cudaMemcpyHostToDevice));
-    gadget_digits_kernel<<<grid1d(rows * len), 256>>>(log2_q, bg_log, levels, (const int64_t*)dx.p, rows, len,
-                                                     (int64_t*)dd.p);
-    CU(cudaGetLastError());
-    CU(cudaMemcpy(digits, dd.p, in_bytes * levels, cudaMemcpyDeviceToHost));
-    return FDSNN_OK;
+    return guarded([&]() -> int {
+        if (log2_q < 1 || log2_q > 62 || bg_log < 1 || levels < 1 || (int64_t)bg_log * levels > 63)
+            return set_err(FDSNN_ERR_PARAMETER, "gadget: q=2^%d, B=2^%d, levels=%d unsupported", log2_q, bg_log, levels);
+        if (rows < 0 || len < 0 || (rows * len > 0 && (!x || !digits))) return set_err(FDSNN_ERR_PARAMETER, "bad argument");
+        if (rows * len == 0) return FDSNN_OK;
+        if (int rc = ring_device(device)) return rc;
+        const size_t in_bytes = (size_t)rows * len * sizeof(int64_t);
+        DevScratch dx, dd;
+        CU(cudaMalloc(&dx.p, in_bytes));
+        CU(cudaMalloc(&dd.p, in_bytes * levels));
+        CU(cudaMemcpy(dx.p, x, in_bytes, cudaMemcpyHostToDevice));
+        gadget_digits_kernel<<<grid1d(rows * len), 256>>>(log2_q, bg_log, levels, (const int64_t*)dx.p, rows, len,
+                                                         (int64_t*)dd.p);
+        CU(cudaGetLastError());
+        CU(cudaMemcpy(digits, dd.p, in_bytes * levels, cudaMemcpyDeviceToHost));
+        return FDSNN_OK;
+    });
 }
 
 }  // extern "C"

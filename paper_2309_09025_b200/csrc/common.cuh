@@ -20,7 +20,7 @@ struct DevParams {
     int stride;     // LWE row stride in words (>= n+1, multiple of 4)
     int ext_stride; // extracted z-LWE row stride (>= N+1, multiple of 4)
     int p;          // message modulus
-    int half_slot;  // N / p (bootstrap.py:526 half-slot offset)
+    int half_slot;  // N / p (bootstrap.py:333 half-slot offset)
 };
 
 FDSNN_DEV double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -78,20 +78,8 @@ FDSNN_DEV long long round_half_away(double x) {
 // round-to-nearest-even (one F2I) selects the same integer as the reference's
 // round-half-away (ring.py:36-42) -- the two differ only at exact .5 ties.
 FDSNN_DEV long long round_product(double x) { return __double2ll_rn(x); }
-// Low 32 bits of the same rounding.  FDSNN_MAGIC_ROUND=1 rounds with one DADD
-// of 1.5 * 2^52 (for |x| < 2^51 the sum's ulp is 1, so the FP64 unit's
-// round-to-nearest-even picks the same integer as F2I.RN and the low mantissa
-// word holds it mod 2^32) instead of an F2I on the conversion pipe.
-#ifndef FDSNN_MAGIC_ROUND
-#define FDSNN_MAGIC_ROUND 0
-#endif
-FDSNN_DEV uint32_t round_lo32(double x) {
-#if FDSNN_MAGIC_ROUND
-    return (uint32_t)__double2loint(x + 6755399441055744.0);
-#else
-    return (uint32_t)__double2ll_rn(x);
-#endif
-}
+// Low 32 bits of the same rounding (the accumulator update is mod q <= 2^31).
+FDSNN_DEV uint32_t round_lo32(double x) { return (uint32_t)__double2ll_rn(x); }
 
 FDSNN_DEV void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -26,6 +26,11 @@ inline std::string fdsn_read(const char* path, const char* kind, const char* dig
     FILE* f = std::fopen(path, "rb");
     if (!f) return std::string("cannot open ") + path;
     struct Closer { FILE* f; ~Closer() { std::fclose(f); } } closer{f};
+    // the file may come from outside: every extent is checked against the
+    // bytes actually left in the file before anything is allocated
+    if (std::fseek(f, 0, SEEK_END) != 0) return "cannot seek";
+    const long fsize = std::ftell(f);
+    if (fsize < 0 || std::fseek(f, 0, SEEK_SET) != 0) return "cannot seek";
     auto rd = [&](void* p, size_t n) { return std::fread(p, 1, n, f) == n; };
     char magic[4];
     if (!rd(magic, 4) || std::memcmp(magic, "FDSN", 4) != 0) return "not an FDSN container";
@@ -60,8 +65,11 @@ inline std::string fdsn_read(const char* path, const char* kind, const char* dig
         for (int i = 0; i < nd; ++i) {
             if (!rd(&a.shape[i], 8)) return "truncated container";
             if (a.shape[i] < 0) return "negative array extent";
+            if (a.shape[i] > 0 && count > (INT64_MAX / 8) / a.shape[i]) return "array extent overflow";
             count *= a.shape[i];
         }
+        const long pos = std::ftell(f);
+        if (pos < 0 || count > (int64_t)(fsize - pos) / 8) return "truncated container";
         a.data.resize((size_t)count);
         if (count && !rd(a.data.data(), (size_t)count * 8)) return "truncated container";
         out[tag] = std::move(a);

@@ -1,6 +1,6 @@
 // keyswitch.cuh — batched LWE key switching z (dim N) -> s (dim n).
 //
-// Reference: bootstrap.key_switch_batch (bootstrap.py:496-509) with
+// Reference: bootstrap.key_switch_batch (bootstrap.py:303-316) with
 // rgsw.gadget_decompose (rgsw.py:119-133):
 //   digits of centred a_j, base 2^ks_log, ks_L levels, lowest first,
 //   flattened index j*ks_L + t;

@@ -1,6 +1,6 @@
 // ks_umma.cuh — LWE key switching on the 5th-generation tensor cores.
 //
-// Reference: bootstrap.key_switch_batch (bootstrap.py:496-509) with the
+// Reference: bootstrap.key_switch_batch (bootstrap.py:303-316) with the
 // gadget rule of rgsw.gadget_decompose (rgsw.py:119-133):
 //   out_a = -sum_k dig[v][k] * kskA[k][c]   (mod q),  k = j*ks_L + t.
 // The mask part is an integer GEMM  C = D (V x K) . KSK (K x n)  with

@@ -2,12 +2,12 @@
 // GINX blind rotation, sample extract.  Key switching is keyswitch.cuh.
 //
 // Reference semantics (all bit-exact):
-//   bootstrap_batch      bootstrap.py:517-534
+//   bootstrap_batch      bootstrap.py:324-341
 //   rescale              ring.py:56-67   (a2N, b2N (+N//p half-slot, :526))
-//   accumulator init     bootstrap.py:527-529, monomial_rotate_raw ring.py:226-242
-//   CMux step i          _fold_twist_kernel bootstrap.py:386-423,
-//                        einsum MAC :472, _untwist_round_add_kernel :425-442
-//   sample extract       bootstrap.py:484-488
+//   accumulator init     bootstrap.py:334-336, monomial_rotate_raw ring.py:226-242
+//   CMux step i          _fold_twist_kernel bootstrap.py:193-230,
+//                        einsum MAC :279, _untwist_round_add_kernel :232-249
+//   sample extract       bootstrap.py:291-295
 //
 // Work decomposition: one group of T = M/8 threads owns one accumulator
 // (2 x N int32 in shared memory) for all n CMux steps; G = 256/T groups per
@@ -31,7 +31,6 @@
 // untwist is a multiply by conj(twist).
 #pragma once
 #include "fft.cuh"
-#include "fft2.cuh"
 #ifndef FDSNN_SKIP_ENTRY
 #define FDSNN_SKIP_ENTRY 1
 #endif
@@ -40,9 +39,6 @@
 #endif
 #ifndef FDSNN_SKEW
 #define FDSNN_SKEW 2  // start half the accumulators of a CTA late: 1 = one transform pair, 2 = ~0.6 pair
-#endif
-#ifndef FDSNN_LY2
-#define FDSNN_LY2 0  // layout-2 transforms (fft2.cuh): bit-exact, 2.5% slower on B200 (DESIGN 8)
 #endif
 
 namespace fdsnn {
@@ -77,12 +73,10 @@ struct PbsShape {
     static constexpr int PADM = M == 1024 ? FFT1024_HALF + 576 : M + M / 8;
 };
 
-// LY2 (layout-2 transforms, fft2.cuh): + the warp-local E1 region
-__host__ __device__ constexpr int acc_words(int N, bool) { return N; }
 template <int M>
-__host__ __device__ constexpr size_t pbs_group_bytes(int N, int n, bool ly2 = false) {
-    return (ly2 ? 3 : 2) * PbsShape<M>::PADM * sizeof(double2)   // exchange buffers
-           + 2 * (size_t)acc_words(N, ly2) * sizeof(int32_t)      // accumulator
+__host__ __device__ constexpr size_t pbs_group_bytes(int N, int n) {
+    return 2 * PbsShape<M>::PADM * sizeof(double2)   // exchange buffers
+           + 2 * (size_t)N * sizeof(int32_t)          // accumulator
            + (((size_t)n * sizeof(uint16_t) + 15) & ~(size_t)15);  // a2N
 }
 
@@ -93,9 +87,6 @@ constexpr int PBS_THREADS = 256;
 constexpr size_t PBS_GROUP_PAD = 64;
 #ifndef FDSNN_ILV
 #define FDSNN_ILV 1  // M = 512, G = 4: accumulator pairs interleaved lane by lane (key loads broadcast)
-#endif
-#ifndef FDSNN_MAGIC_I2F
-#define FDSNN_MAGIC_I2F 0  // digit -> double by exponent bits + one DADD instead of I2F.F64
 #endif
 #ifndef FDSNN_RING_S
 #define FDSNN_RING_S 5
@@ -109,8 +100,8 @@ __host__ __device__ constexpr size_t pbs_chunk_bytes() { return (size_t)2 * M * 
 template <int M>
 __host__ __device__ constexpr int pbs_stages(int G) { return G >= 6 ? 3 : PbsRing<M>::S; }
 template <int M>
-__host__ __device__ constexpr size_t pbs_smem_bytes(int G, int N, int n, bool ly2 = false) {
-    return 128 + (size_t)pbs_stages<M>(G) * pbs_chunk_bytes<M>() + (size_t)G * (pbs_group_bytes<M>(N, n, ly2) + PBS_GROUP_PAD);
+__host__ __device__ constexpr size_t pbs_smem_bytes(int G, int N, int n) {
+    return 128 + (size_t)pbs_stages<M>(G) * pbs_chunk_bytes<M>() + (size_t)G * (pbs_group_bytes<M>(N, n) + PBS_GROUP_PAD);
 }
 
 template <int M>
@@ -184,8 +175,7 @@ template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN, bool PAIR = false, int
 __global__ void __launch_bounds__(G * (M / 8), 1)
 pbs_blind_rotate_kernel(const PbsArgs args) {
     constexpr uint32_t TMEM_COLS = PAIR ? 512 : PBS_TMEM_COLS;
-    constexpr bool LY2 = PAIR && M == 512 && FDSNN_LY2;
-    constexpr int NA = acc_words(2 * M, LY2);  // words per accumulator poly
+    constexpr int NA = 2 * M;  // words per accumulator poly
     constexpr int T = M / 8;
     constexpr int PADM = PbsShape<M>::PADM;
     constexpr int S = pbs_stages<M>(G);
@@ -206,21 +196,16 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     // ILV: groups 2h and 2h+1 share warps 4h..4h+3, lane parity = group, so
     // the two lanes of a pair hold the same t and their key-slice loads in the
     // MAC hit one address (a broadcast: half the shared-memory wavefronts).
-    constexpr bool ILV = FDSNN_ILV && M == 512 && G == 4 && PAIR && !LY2;
+    constexpr bool ILV = FDSNN_ILV && M == 512 && G == 4 && PAIR;
     const int g = ILV ? 2 * (threadIdx.x / (2 * T)) + (threadIdx.x & 1) : threadIdx.x / T;
     const int t = ILV ? (threadIdx.x % (2 * T)) >> 1 : threadIdx.x % T;
-    unsigned char* mine = smem_raw + 128 + S * CHUNK + g * (pbs_group_bytes<M>(N, n, LY2) + PBS_GROUP_PAD);
+    unsigned char* mine = smem_raw + 128 + S * CHUNK + g * (pbs_group_bytes<M>(N, n) + PBS_GROUP_PAD);
     double2* buf0 = reinterpret_cast<double2*>(mine);
     double2* buf1 = buf0 + PADM;
-    double2* xbuf = buf1 + PADM;  // LY2: warp-local E1 regions (2 x 288)
-    int32_t* acc = reinterpret_cast<int32_t*>(LY2 ? xbuf + PADM : buf1 + PADM);  // [2][NA]
+    int32_t* acc = reinterpret_cast<int32_t*>(buf1 + PADM);  // [2][NA]
     uint16_t* a2N = reinterpret_cast<uint16_t*>(acc + 2 * NA);
-    // accumulator word of coefficient j.  LY2 swizzles bit 2 with bit 5: a
-    // warp's layout-2 set {c + 8a + b : a < 8, b < 4} rotated by any k then
-    // hits 32 distinct banks.  The swizzle commutes with adding multiples of
-    // 64, so per-thread offsets r*T + h*M (T = 64) stay compile-time.
-    auto ax = [&](int j) { return LY2 ? j ^ ((j >> 3) & 4) : j; };
-    auto coef = [&](int r, int h) { return (LY2 ? l2::fa_n(t, r) : t + r * T) + h * M; };
+    auto ax = [&](int j) { return j; };  // accumulator word of coefficient j
+    auto coef = [&](int r, int h) { return t + r * T + h * M; };
 
     const int64_t V = (int64_t)args.nlut * args.count;
     const int64_t v0 = args.v_base + (int64_t)blockIdx.x * G;
@@ -248,21 +233,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
     // ---- per-thread constants -> TMEM (warps 0-3 cover all lane quadrants)
     if (warp < 4 && active) {
         double2 twist[8];
-        if constexpr (LY2) {
-            // w64^(n1 k0) (n1 = 1..7) and w512^(n0 (k0 + 8 k1)) of the fB lane
-            const double2* t64 = args.tables + M + twiddle_table_size<M>();
-            const double2* t512 = t64 + 64;
-            const int k0 = l2::fb_k0(t), n0 = l2::fb_n0(t);
-            double2 c[8];
-#pragma unroll
-            for (int n1 = 0; n1 < 8; ++n1) c[n1] = __ldg(t64 + (((n1 + 1) * k0) & 63));
-            tmem_st_c8(lane_base, c);
-#pragma unroll
-            for (int k1 = 0; k1 < 8; ++k1) c[k1] = __ldg(t512 + ((n0 * (k0 + 8 * k1)) & 511));
-            tmem_st_c8(lane_base + 32, c);
-#pragma unroll
-            for (int r = 0; r < 8; ++r) twist[r] = __ldg(args.tables + l2::fa_n(t, r));
-        } else {
+        {
             tmem_store_twiddles<M>(lane_base, t, args.tables);
             load_twist<M>(twist, t, args.tables);
         }
@@ -340,8 +311,6 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
         gs.sync();
         const uint32_t own_col = lane_base + PBS_TMEM_OWN + 32 * (uint32_t)(warp / 4);
         const uint32_t o_col = lane_base + 256 + 64 * (uint32_t)(warp / 4);  // PAIR only
-        const uint32_t x_col = lane_base + 384 + 32 * (uint32_t)(warp / 4);  // LY2: E1 TMEM hops
-        const TwiddlesL2 tw2{lane_base};
         {
             uint32_t w[32];
 #pragma unroll
@@ -442,25 +411,11 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     const int ca = fa / LQ, la = fa % LQ, cb = fb / LQ, lb = fb % LQ;
                     if (pr == LQ / 2) make_x(1, xlo[1], xhi[1]);  // first pair touching poly 1
                     double2 v0[8], v1[8];
-                    constexpr bool FT = FDSNN_FUSED_TW && !LY2;
+                    constexpr bool FT = FDSNN_FUSED_TW;
                     double2 twv[8];
                     {
                         uint32_t twr[32];
                         tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
-#if FDSNN_MAGIC_I2F
-                        // digit fields as doubles without the conversion pipe:
-                        // bits (0x43300000, f) = 2^52 + f, minus (2^52 + B/2 - 1)
-                        const double dmag = 4503599627370496.0 + (double)halfB1;
-                        auto i2d = [&](uint32_t f) { return __hiloint2double(0x43300000, (int)f) - dmag; };
-                        uint32_t d1[8], d2[8], e1[8], e2[8];
-#pragma unroll
-                        for (int r = 0; r < 8; ++r) {
-                            d1[r] = ((uint32_t)xlo[ca][r] >> (bg * la)) & bmask;
-                            d2[r] = ((uint32_t)xhi[ca][r] >> (bg * la)) & bmask;
-                            e1[r] = ((uint32_t)xlo[cb][r] >> (bg * lb)) & bmask;
-                            e2[r] = ((uint32_t)xhi[cb][r] >> (bg * lb)) & bmask;
-                        }
-#else
                         auto i2d = [](int32_t d) { return (double)d; };
                         int32_t d1[8], d2[8], e1[8], e2[8];
 #pragma unroll
@@ -470,7 +425,6 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                             e1[r] = ((xlo[cb][r] >> (bg * lb)) & bmask) - halfB1;
                             e2[r] = ((xhi[cb][r] >> (bg * lb)) & bmask) - halfB1;
                         }
-#endif
                         tmem_wait32(twr);
 #pragma unroll
                         for (int r = 0; r < 8; ++r) {
@@ -493,10 +447,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                         mbar_wait(&full[s0], (uint32_t)((c / S) & 1));
                         mbar_wait(&full[s1], (uint32_t)(((c + 1) / S) & 1));
                     };
-                    if constexpr (LY2) {
-                        fft2_fwd_pair(v0, v1, t, tw2, xbuf, buf0, buf1, x_col, gs);
-                        keys_ready();
-                    } else if constexpr (FDSNN_EARLY_KEYS) {
+                    if constexpr (FDSNN_EARLY_KEYS) {
                         // the first pair of a step follows the step's closing
                         // barrier, which already fences the buffers' last readers
                         if (pr == 0 && FDSNN_SKIP_ENTRY)
@@ -598,8 +549,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
                     tmem_ld32_async(lane_base + PBS_TMEM_TWIST, twr);
                     tmem_ld32_async(own_col, own);
                 };
-                if constexpr (LY2) fft2_inv_pair(O0, O1, t, tw2, xbuf, buf0, buf1, x_col, gs, fetch);
-                else fft_group2<M, true>(O0, O1, t, tw, buf0, buf1, gs, fetch);
+                fft_group2<M, true>(O0, O1, t, tw, buf0, buf1, gs, fetch);
                 tmem_wait32(twr);
                 tmem_touch32(own);
 #pragma unroll
@@ -644,7 +594,7 @@ pbs_blind_rotate_kernel(const PbsArgs args) {
             int32_t* a_dst = args.acc_io + v * 2 * N;
             for (int j = t; j < 2 * N; j += T) a_dst[j] = acc[(j >= N ? NA : 0) + ax(j & (N - 1))];
         } else {
-            // sample extract (bootstrap.py:484-488): (a_0, -a_{N-1}, ..., -a_1), b = acc_b[0]
+            // sample extract (bootstrap.py:291-295): (a_0, -a_{N-1}, ..., -a_1), b = acc_b[0]
             uint32_t* out = args.ext_out + v * prm.ext_stride;
             for (int j = t; j < N; j += T) {
                 const uint32_t a = (j == 0) ? (uint32_t)acc[0] : ((uint32_t)(-acc[ax(N - j)]) & qmask);
@@ -931,7 +881,7 @@ __host__ __device__ constexpr size_t pbs_wide_smem_bytes(int L2, int N, int n) {
 }
 
 // Fourier transform of the bootstrapping key rows (BootstrapKey.__init__,
-// bootstrap.py:319-323): centred residues -> fold, twist, forward DFT, then
+// bootstrap.py:125-130): centred residues -> fold, twist, forward DFT, then
 // scaled by 1/M (exact) for the untwist-free epilogue above.
 // One group of T threads per polynomial; G polys per CTA.
 template <int M, int G>

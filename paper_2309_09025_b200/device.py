@@ -76,6 +76,14 @@ class DeviceContext:
         _lib.check(self.lib.fdsnn_bsk_load(self.h, _ptr(rows), _ptr(ksk_A), _ptr(ksk_b)))
         self.keys_loaded = True
 
+    def load_key_switch_key(self, ksk_A: np.ndarray, ksk_b: np.ndarray) -> None:
+        """Only the key-switch key (no bootstrapping key is stored or transformed)."""
+        p = self.params
+        ksk_A, ksk_b = _i64(ksk_A), _i64(ksk_b)
+        if ksk_A.shape != (p.N * p.ks_levels, p.n) or ksk_b.shape != (p.N * p.ks_levels,):
+            raise ParameterError("key-switch key shape does not match params")
+        _lib.check(self.lib.fdsnn_ksk_load(self.h, _ptr(ksk_A), _ptr(ksk_b)))
+
     def load_keys_fdsn(self, path: str) -> None:
         """Bootstrapping + key-switch key straight from a reference FDSN BK file."""
         _lib.check(self.lib.fdsnn_bsk_load_fdsn(self.h, str(path).encode(),
@@ -127,8 +135,11 @@ class DeviceContext:
             cnt, *[_ptr(o) for o in out]))
         return tuple(out)
 
-    def blind_rotate_batch(self, acc, a2N):
-        acc = _i64(acc).copy()
+    def blind_rotate_batch(self, acc: np.ndarray, a2N):
+        """Rotates the C-contiguous int64 `acc` in place (the C entry point
+        writes the results back into the caller's buffer) and returns it."""
+        if acc.dtype != np.int64 or not acc.flags.c_contiguous or not acc.flags.writeable:
+            raise ParameterError("accumulator must be a writeable C-contiguous int64 array")
         a2N = _i64(a2N)
         _lib.check(self.lib.fdsnn_blind_rotate_batch(self.h, _ptr(acc), _ptr(a2N), acc.shape[0]))
         return acc

@@ -8,7 +8,7 @@ reference.  Run:
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
         python tests/golden/make_golden.py [section ...]
 
-Sections: keys toy toy64 desk c4 layer config0 config1 config2 fdsn plain paper ring
+Sections: keys toy toy64 desk c4 layer config0 config1 config2 config4 fdsn plain paper ring
 """
 
 from __future__ import annotations
@@ -225,14 +225,38 @@ def sec_config2():
          boots=np.array([stats.bootstrap_count]), ref_seconds=np.array([dt]), **spikes)
 
 
+def sec_config4():
+    """Config 4 (C4 params, p=4096): one synthetic image through
+    conv(8x5x5)->LIF->FC 4608->256->LIF->256->128->LIF->128->10->LIF, T=8,
+    through the reference's encrypted infer (network.py:459-491), 80,032 PBS."""
+    prm = W.c4_params(fdsnn)
+    sk, zk, bsk = W.keys(fdsnn, prm, 0)
+    lif = W.lif_for(fdsnn, prm)
+    net = W.config4_network(fdsnn, lif)
+    imgs = W.synth_images(32)
+    encs = W.encrypt_images(fdsnn, prm, sk, imgs[:1])
+    spikes = {}
+
+    def obs(li, t, x):
+        spikes[f"l{li}_t{t}"] = fdsnn.lwe.decrypt_batch(x.A, x.b, sk, prm)
+
+    t0 = time.time()
+    scores, stats = fdsnn.network.infer(encs[0], net, bsk, workers=8, observer=obs)
+    dt = time.time() - t0
+    print(f"config4 image 0: {stats.bootstrap_count} PBS in {dt:.1f}s")
+    save("config4_img0", scores=fdsnn.lwe.decrypt_batch(scores.A, scores.b, sk, prm),
+         score_digest=np.frombuffer(bytes.fromhex(sha(scores.A, scores.b)), np.uint8),
+         boots=np.array([stats.bootstrap_count]), ref_seconds=np.array([dt]), **spikes)
+
+
 def sec_plain():
     """Reference oracle.plain_infer (oracle.py:44-78) on the config 2 network
-    (32 synthetic images, T=4) and the config 4 network (4 images, T=8):
+    (32 synthetic images, T=4) and the config 4 network (32 images, T=8):
     integer scores and per-layer spike counts, plus whether the strict range
     check at p raises."""
     out = {}
     for tag, prm, mk, nimg in (("c2", W.desk1024(fdsnn), W.config2_network, 32),
-                               ("c4", W.c4_params(fdsnn), W.config4_network, 4)):
+                               ("c4", W.c4_params(fdsnn), W.config4_network, 32)):
         lif = W.lif_for(fdsnn, prm)
         net = mk(fdsnn, lif)
         imgs = W.synth_images(nimg).astype(np.float64) / 255.0
@@ -357,9 +381,10 @@ SECTIONS = {
     "desk": lambda: sec_lif(W.desk1024(fdsnn), "desk_lif", 32),
     "c4": lambda: sec_lif(W.c4_params(fdsnn), "c4_lif", 4),
     "layer": sec_layer, "config0": sec_config0, "config1": sec_config1, "config2": sec_config2,
+    "config4": sec_config4,
     "plain": sec_plain, "paper": sec_paper, "ring": sec_ring,
 }
 
 if __name__ == "__main__":
-    for name in sys.argv[1:] or [k for k in SECTIONS if k != "config2"]:
+    for name in sys.argv[1:] or [k for k in SECTIONS if k not in ("config2", "config4")]:
         SECTIONS[name]()

@@ -45,6 +45,11 @@ def test_library_binds_and_reports_errors_without_gpu():
     assert b"ring degree" in lib.fdsnn_last_error()
     prm = _lib.FdsnnParams(512, 1024, 25, 1024, 7, 3, 5, 5)  # gadget does not cover q
     assert lib.fdsnn_ctx_create(ctypes.byref(prm), 0, ctypes.byref(h)) == _lib.FDSNN_ERR_PARAMETER
+    # covers q, but y = centred(x) + (B/2-1)(1+B+B^2) overflows the int32
+    # digit arithmetic of the rotation kernels: rejected, not silently wrong
+    prm = _lib.FdsnnParams(512, 1024, 27, 1024, 11, 3, 3, 9)
+    assert lib.fdsnn_ctx_create(ctypes.byref(prm), 0, ctypes.byref(h)) == _lib.FDSNN_ERR_PARAMETER
+    assert b"int32 digit range" in lib.fdsnn_last_error()
 
 
 def test_no_device_fails_loudly():

@@ -40,9 +40,10 @@ def test_identity_rotation_steps(toy, toy_keys):
     a2N = rng.integers(0, 2 * toy.N, (9, toy.n))
     a2N[:, ::2] = 0
     a2N[3] = 0
+    orig = acc.copy()
     got = bootstrap.blind_rotate_batch(acc, a2N, bsk)
-    assert np.array_equal(got, O.blind_rotate(acc, a2N, oracle_key(toy, bsk)))
-    assert np.array_equal(got[3], acc[3])
+    assert np.array_equal(got, O.blind_rotate(orig, a2N, oracle_key(toy, bsk)))
+    assert np.array_equal(got[3], orig[3])
 
 
 def test_deterministic(desk, desk_keys):
@@ -190,8 +191,98 @@ def test_desk_blind_rotate_raw_mode(desk, desk_keys, count):
     acc = rng.integers(0, desk.q, (count, 2, desk.N))
     a2N = rng.integers(0, 2 * desk.N, (count, desk.n))
     a2N[::3, 0] = 0
+    orig = acc.copy()
     got = bootstrap.blind_rotate_batch(acc, a2N, bsk)
     key = oracle_key(desk, bsk)
     for j in sorted({0, 1, 3, count // 2, count - 1}):
-        want = O.blind_rotate(acc[j:j + 1], a2N[j:j + 1], key)
+        want = O.blind_rotate(orig[j:j + 1], a2N[j:j + 1], key)
         assert np.array_equal(got[j:j + 1], want), j
+
+
+@pytest.mark.gpu
+def test_fdsn_hostile_containers_fail_cleanly(toy, toy_keys, tmp_path):
+    """The C reader checks every extent against the bytes left in the file and
+    the body array against the mask count: a bogus shape is a ParameterError,
+    not an abort (bad_alloc) or a heap over-read."""
+    import struct
+    from paper_2309_09025_b200 import serial
+    from paper_2309_09025_b200.device import DeviceContext
+    sk, _, bsk = toy_keys
+    rng = np.random.default_rng(14)
+    A, b = lwe.encrypt_batch(rng.integers(-3, 5, 6), sk, toy, rng)
+    good = tmp_path / "ct.bin"
+    serial.save_ciphertexts(good, network.CiphertextTensor((6,), A, b, toy.q), toy)
+    blob = good.read_bytes()
+    dev = DeviceContext(toy)
+
+    def header_end():
+        return 9 + blob[8]
+
+    # 1. first array declares 2^40 x 2^20 elements
+    bad = bytearray(blob)
+    pos = header_end()
+    tl = bad[pos]
+    struct.pack_into("<q", bad, pos + 2 + tl, 1 << 40)
+    (tmp_path / "huge.bin").write_bytes(bytes(bad))
+    with pytest.raises(errors.ParameterError):
+        serial.load_ciphertexts_device(tmp_path / "huge.bin", dev)
+    # 2. body array "b" of shape (6, 0): zero payload but 6 ciphertexts claimed
+    ct = tmp_path / "b0.bin"
+    with open(ct, "wb") as f:
+        serial._header(f, serial.KIND_CIPHERTEXTS, toy)
+        serial._put(f, "shape", np.asarray([6]))
+        serial._put(f, "A", A)
+        serial._put(f, "b", np.zeros((6, 0), np.int64))
+    with pytest.raises(errors.ParameterError):
+        serial.load_ciphertexts_device(ct, dev)
+    # 3. truncated key container
+    bk = tmp_path / "bk.bin"
+    serial.save_bootstrap_key(bk, bsk)
+    kb = bk.read_bytes()
+    (tmp_path / "bk_cut.bin").write_bytes(kb[: len(kb) // 2])
+    with pytest.raises(errors.ParameterError):
+        serial.load_bootstrap_key_device(tmp_path / "bk_cut.bin", toy)
+    # the context still works afterwards
+    rows, shape = serial.load_ciphertexts_device(good, dev)
+    assert shape == (6,)
+    A2, b2 = dev.rows_to_host(rows)
+    assert np.array_equal(A2, A % toy.q) and np.array_equal(b2, b % toy.q)
+
+
+@pytest.mark.gpu
+def test_host_boundary_concurrent_streams(desk, desk_keys):
+    """int64 host <-> device rows from several host threads on different
+    streams at once (each stream has its own page-locked slots), sizes that
+    span several slots, interleaved with bootstraps on the context stream."""
+    import threading
+    import torch
+    sk, _, bsk = desk_keys
+    dev = bsk.device
+    rng = np.random.default_rng(15)
+    sizes = [1, 5000, 9000, 777]
+    data = [(rng.integers(-(1 << 40), 1 << 40, (c, desk.n)), rng.integers(-(1 << 40), 1 << 40, c)) for c in sizes]
+    errs = []
+
+    def work(k):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for _ in range(3):
+                    A, b = data[k]
+                    rows = dev.rows_from_host(A, b)
+                    A2, b2 = dev.rows_to_host(rows)
+                    assert np.array_equal(A2, A % desk.q) and np.array_equal(b2, b % desk.q)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    g = neuron.g_fire(desk.p)
+    mA, mb = lwe.encrypt_batch(rng.integers(-511, 513, 40), sk, desk, rng)
+    want = bootstrap.bootstrap_batch(g, mA, mb, bsk)
+    ths = [threading.Thread(target=work, args=(k,)) for k in range(len(sizes))]
+    for t in ths:
+        t.start()
+    got = bootstrap.bootstrap_batch(g, mA, mb, bsk)
+    for t in ths:
+        t.join()
+    assert not errs, errs
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])

@@ -48,9 +48,35 @@ def test_blind_rotate_batch(toy, toy_keys):
     acc = rng.integers(0, toy.q, (5, 2, toy.N))
     a2N = rng.integers(0, 2 * toy.N, (5, toy.n))
     a2N[0] = 0  # identity rotation
+    want = O.blind_rotate(acc.copy(), a2N, oracle_key(toy, bsk))
     got = bootstrap.blind_rotate_batch(acc, a2N, bsk)
-    want = O.blind_rotate(acc, a2N, oracle_key(toy, bsk))
     assert np.array_equal(got, want)
+    assert got is acc  # C-contiguous int64: rotated in place (bootstrap.py:263,281)
+
+
+def test_blind_rotate_batch_ownership(toy, toy_keys):
+    """The reference's ownership rules (bootstrap.py:252-282): a C-contiguous
+    int64 accumulator is rotated in place; a non-contiguous one is copied and
+    left alone; when every rotation index is 0 mod 2N no step runs and the
+    accumulators come back unreduced."""
+    sk, zk, bsk = toy_keys
+    rng = np.random.default_rng(41)
+    acc = rng.integers(0, toy.q, (4, 2, toy.N))
+    a2N = rng.integers(0, 2 * toy.N, (4, toy.n))
+    want = O.blind_rotate(acc.copy(), a2N, oracle_key(toy, bsk))
+    wide = np.zeros((4, 2, 2 * toy.N), np.int64)
+    view = wide[:, :, ::2]  # non-contiguous view
+    view[...] = acc
+    got = bootstrap.blind_rotate_batch(view, a2N, bsk)
+    assert got is not view and np.array_equal(got, want)
+    assert np.array_equal(view, acc)  # caller's strided array untouched
+    raw = acc.copy()
+    raw[0, 0, :3] = [-5, toy.q + 7, 3 * toy.q]  # unreduced values
+    zero = np.zeros_like(a2N)
+    zero[1, 0] = 2 * toy.N  # == 0 mod 2N
+    kept = raw.copy()
+    assert bootstrap.blind_rotate_batch(raw, zero, bsk) is raw
+    assert np.array_equal(raw, kept)
 
 
 def test_key_switch_batch(toy, toy_keys):
@@ -61,6 +87,28 @@ def test_key_switch_batch(toy, toy_keys):
     got = bootstrap.key_switch_batch(A, b, bsk.ksk, toy)
     want = O.key_switch(A, b, oracle_key(toy, bsk))
     assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    # bsk.ksk is served by the bootstrapping key's own context
+    assert bootstrap._key_device(bsk.ksk, toy) is bsk.device
+
+
+def test_key_switch_standalone_key(toy, toy_keys):
+    """A KeySwitchKey not attached to a loaded BootstrapKey gets a context that
+    holds only the key-switch key; the cache entry dies with the key."""
+    import gc
+    sk, zk, bsk = toy_keys
+    ksk = bootstrap.KeySwitchKey(bsk.ksk.A.copy(), bsk.ksk.b.copy(), bsk.ksk.base, bsk.ksk.levels, bsk.ksk.N)
+    rng = np.random.default_rng(6)
+    A = rng.integers(-toy.q, toy.q, (7, toy.N))
+    b = rng.integers(0, toy.q, 7)
+    got = bootstrap.key_switch_batch(A, b, ksk, toy)
+    want = O.key_switch(A, b, oracle_key(toy, bsk))
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    ctx = bootstrap._key_device(ksk, toy)
+    assert ctx is not bsk.device and not ctx.keys_loaded
+    before = len(bootstrap._KS_DEVICES)
+    del ksk, ctx
+    gc.collect()
+    assert len(bootstrap._KS_DEVICES) == before - 1
 
 
 @pytest.mark.parametrize("which,count", [("toy", 9), ("desk", 130), ("c4prm", 257)])

@@ -194,6 +194,48 @@ def test_fdsn_containers_byte_identical_to_reference(toy, toy_keys, tmp_path):
         serial.load_secret_key(tmp_path / "ct.bin", toy)
 
 
+def test_fdsn_truncated_containers_raise_serialization_error(toy, toy_keys, tmp_path):
+    """A container cut at any byte (header, tag, shape or payload) raises the
+    reference's SerializationError, never IndexError/struct.error; negative
+    extents are rejected too."""
+    import struct
+    from paper_2309_09025_b200 import serial
+    sk, zk, bsk = toy_keys
+    rng = np.random.default_rng(3)
+    A, b = lwe.encrypt_batch(rng.integers(-3, 5, 3), sk, toy, rng)
+    path = tmp_path / "ct.bin"
+    serial.save_ciphertexts(path, network.CiphertextTensor((3,), A, b, toy.q), toy)
+    blob = path.read_bytes()
+    # array boundaries: a cut there is a well-formed shorter container, whose
+    # missing array is a KeyError in the reference too (serial.py:140-145)
+    bounds, pos = {9 + blob[8]}, 9 + blob[8]
+    while pos < len(blob):
+        tl = blob[pos]
+        nd = blob[pos + 1 + tl]
+        shape = struct.unpack_from(f"<{nd}q", blob, pos + 2 + tl)
+        pos += 2 + tl + 8 * nd + 8 * int(np.prod(shape))
+        bounds.add(pos)
+    cut = tmp_path / "cut.bin"
+    for n in range(len(blob)):
+        cut.write_bytes(blob[:n])
+        want = (errors.SerializationError, KeyError) if n in bounds else errors.SerializationError
+        try:
+            serial.load_ciphertexts(cut, toy)
+        except want:
+            continue
+        except Exception as e:  # pragma: no cover - the failure being tested
+            raise AssertionError(f"cut at {n}: {type(e).__name__}: {e}")
+        raise AssertionError(f"cut at {n} loaded")
+    # a negative extent in the first array header
+    hdr = 9 + blob[8]
+    bad = bytearray(blob)
+    tl = bad[hdr]
+    struct.pack_into("<q", bad, hdr + 1 + tl + 1, -1)
+    cut.write_bytes(bytes(bad))
+    with pytest.raises(errors.SerializationError):
+        serial.load_ciphertexts(cut, toy)
+
+
 def _paper_model():
     from paper_2309_09025_b200 import network as N
     m = np.load(os.path.join(GOLDEN, "paper_model.npz"))

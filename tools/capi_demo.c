@@ -3,7 +3,7 @@
  * (no Python): load a bootstrapping key and a ciphertext tensor from the
  * reference's FDSN containers (serial.save_bootstrap_key / save_ciphertexts),
  * bootstrap every ciphertext through the sign table (neuron.g_fire: test
- * polynomial = Delta everywhere, bootstrap.py:283-289), write the results.
+ * polynomial = Delta everywhere, bootstrap.py:90-96), write the results.
  *
  *   capi_demo BK.bin CT.bin PARAMS_DIGEST n N log2q p bg_log levels ks_log ks_levels OUT.bin
  *
