@@ -135,6 +135,12 @@ int fdsnn_weight_sum(fdsnn_ctx* ctx, const int64_t* M, int64_t out_cells,
  * may be reused, to_host once they are complete.  Thread-safe per context. */
 int fdsnn_rows_from_host(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b,
                          int64_t count, uint32_t* d_rows, void* stream);
+/* Several host arrays stacked in order into one device row buffer (the
+ * batched network calls: no host-side concatenation).  counts[p] rows of
+ * A[p] (counts[p], n) and b[p] (counts[p],). */
+int fdsnn_rows_from_host_parts(fdsnn_ctx* ctx, int32_t nparts, const int64_t* const* A,
+                               const int64_t* const* b, const int64_t* counts, uint32_t* d_rows,
+                               void* stream);
 int fdsnn_rows_to_host(fdsnn_ctx* ctx, const uint32_t* d_rows, int64_t count,
                        int64_t* A, int64_t* b, void* stream);
 

@@ -55,6 +55,7 @@ SIGNATURES = {
     "fdsnn_key_switch_batch": (_c_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "fdsnn_weight_sum": (_c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "fdsnn_rows_from_host": (_c_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
+    "fdsnn_rows_from_host_parts": (_c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp]),
     "fdsnn_rows_to_host": (_c_int, [_vp, _vp, _i64, _vp, _vp, _vp]),
     "fdsnn_pbs_dev": (_c_int, [_vp, _i32, _i32p, _i64p, _i64p, _vp, _vp, _i64, _vp, _vp]),
     "fdsnn_operator_load": (_c_int, [_vp, _vp, _i64, _i64, _i32p]),

@@ -726,6 +726,31 @@ int fdsnn_lut_load(fdsnn_ctx* ctx, const int64_t* testpoly, int32_t* lut_id) {
     });
 }
 
+int fdsnn_rows_from_host_parts(fdsnn_ctx* ctx, int32_t nparts, const int64_t* const* A,
+                               const int64_t* const* b, const int64_t* counts, uint32_t* d_rows, void* stream) {
+    return guarded([&]() -> int {
+        if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");
+        if (nparts < 0 || (nparts > 0 && (!A || !b || !counts))) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        std::vector<HostPart> parts;
+        int64_t total = 0;
+        for (int32_t p = 0; p < nparts; ++p) {
+            if (counts[p] < 0) return set_err(FDSNN_ERR_PARAMETER, "negative count");
+            if (counts[p] == 0) continue;
+            if (!A[p] || !b[p]) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+            parts.push_back({A[p], b[p], counts[p]});
+            total += counts[p];
+        }
+        if (total == 0) return FDSNN_OK;
+        if (!d_rows) return set_err(FDSNN_ERR_PARAMETER, "null argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CU(cudaSetDevice(ctx->device));
+        cudaStream_t s = pick(ctx, stream);
+        const DevParams& d = ctx->dp;
+        CU(upload_parts(ctx->scratch[s].pin, parts.data(), (int)parts.size(), d.n, d.stride, d.qmask, d_rows, s));
+        return FDSNN_OK;
+    });
+}
+
 int fdsnn_rows_from_host(fdsnn_ctx* ctx, const int64_t* A, const int64_t* b, int64_t count,
                          uint32_t* d_rows, void* stream) {
     return guarded([&]() -> int {

@@ -13,8 +13,10 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -24,7 +26,11 @@
 namespace fdsnn {
 
 // Fixed pool of worker threads; parallel_for(n, fn) runs fn(i) for i < n and
-// returns when all are done.  Calls are serialised (one job at a time).
+// returns when all are done.  Calls are serialised (one job at a time).  Idle
+// workers spin briefly before sleeping, so the back-to-back jobs of one
+// transfer (one per staging slot) do not pay a wake-up each.  Each job is a
+// shared object: a worker that picks up a job late only finds its items all
+// claimed (it never touches the caller's function after the caller returned).
 class HostPool {
   public:
     static HostPool& get() {
@@ -39,33 +45,37 @@ class HostPool {
             for (int64_t i = 0; i < n; ++i) fn(i);
             return;
         }
-        std::lock_guard<std::mutex> job(job_mu_);
+        std::lock_guard<std::mutex> serial(job_mu_);
+        auto job = std::make_shared<Job>();
+        job->fn = &fn;
+        job->total = n;
         {
             std::lock_guard<std::mutex> lk(mu_);
-            fn_ = &fn;
-            total_ = n;
-            next_ = 0;
-            done_ = 0;
-            ++gen_;
+            current_ = job;
+            gen_.fetch_add(1, std::memory_order_release);
         }
         cv_.notify_all();
-        run_items();  // the caller works too
-        std::unique_lock<std::mutex> lk(mu_);
-        done_cv_.wait(lk, [&] { return done_ == total_; });
-        fn_ = nullptr;
+        run(*job);  // the caller works too
+        while (job->done.load(std::memory_order_acquire) != n) std::this_thread::yield();
     }
 
     ~HostPool() {
         {
             std::lock_guard<std::mutex> lk(mu_);
             stop_ = true;
-            ++gen_;
+            gen_.fetch_add(1, std::memory_order_release);
         }
         cv_.notify_all();
         for (auto& t : workers_) t.join();
     }
 
   private:
+    struct Job {
+        const std::function<void(int64_t)>* fn = nullptr;
+        int64_t total = 0;
+        std::atomic<int64_t> next{0}, done{0};
+    };
+
     HostPool() {
         cpu_set_t set;
         int cores = 1;
@@ -74,53 +84,49 @@ class HostPool {
         for (int i = 0; i < nthreads; ++i) workers_.emplace_back([this] { loop(); });
     }
 
-    void run_items() {
-        for (;;) {
-            int64_t i;
-            const std::function<void(int64_t)>* f;
-            {
-                std::lock_guard<std::mutex> lk(mu_);
-                if (!fn_ || next_ >= total_) return;
-                i = next_++;
-                f = fn_;
-            }
-            (*f)(i);
-            std::lock_guard<std::mutex> lk(mu_);
-            if (++done_ == total_) done_cv_.notify_all();
+    static void run(Job& job) {
+        for (int64_t i; (i = job.next.fetch_add(1, std::memory_order_relaxed)) < job.total;) {
+            (*job.fn)(i);
+            job.done.fetch_add(1, std::memory_order_release);
         }
     }
 
     void loop() {
         uint64_t seen = 0;
         for (;;) {
+            for (int spin = 0; gen_.load(std::memory_order_acquire) == seen && spin < 20000; ++spin)
+                std::this_thread::yield();
+            std::shared_ptr<Job> job;
             {
                 std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+                seen = gen_.load(std::memory_order_acquire);
                 if (stop_) return;
-                seen = gen_;
+                job = current_;
             }
-            run_items();
+            if (job) run(*job);
         }
     }
 
     std::vector<std::thread> workers_;
     std::mutex mu_, job_mu_;
-    std::condition_variable cv_, done_cv_;
-    const std::function<void(int64_t)>* fn_ = nullptr;
-    int64_t total_ = 0, next_ = 0, done_ = 0;
-    uint64_t gen_ = 0;
+    std::condition_variable cv_;
+    std::shared_ptr<Job> current_;
+    std::atomic<uint64_t> gen_{0};
     bool stop_ = false;
 };
 
-// Page-locked staging: two slots used alternately, each guarded by an event
-// recorded after the DMA that last used it.
+// Page-locked staging: a ring of NSLOT slots, each guarded by an event
+// recorded after the DMA that last used it (so up to NSLOT-1 DMAs are in
+// flight while the pool packs / unpacks the next slot).
 struct PinnedSlots {
-    static constexpr size_t SLOT_BYTES = 8u << 20;
-    void* slot[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
+    static constexpr int NSLOT = 4;
+    static constexpr size_t SLOT_BYTES = 2u << 20;
+    void* slot[NSLOT] = {};
+    cudaEvent_t ev[NSLOT] = {};
 
     cudaError_t ensure() {
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NSLOT; ++s) {
             if (!slot[s]) {
                 cudaError_t e = cudaHostAlloc(&slot[s], SLOT_BYTES, cudaHostAllocPortable);
                 if (e != cudaSuccess) return e;
@@ -133,7 +139,7 @@ struct PinnedSlots {
         return cudaSuccess;
     }
     void release() {
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NSLOT; ++s) {
             if (ev[s]) cudaEventSynchronize(ev[s]), cudaEventDestroy(ev[s]);
             if (slot[s]) cudaFreeHost(slot[s]);
             ev[s] = nullptr;
@@ -177,26 +183,44 @@ inline void unpack_rows_host(const uint32_t* src, int64_t r0, int64_t r1, int n,
     });
 }
 
-// int64 host (A, b) -> device uint32 rows, through the pinned slots.  Returns
-// the first CUDA error.  The caller's arrays may be reused when it returns
-// (every slot's contents were packed from them before the return).
-inline cudaError_t upload_rows(PinnedSlots& ps, const int64_t* A, const int64_t* b, int64_t count, int n,
-                               int stride, uint32_t qmask, uint32_t* d_rows, cudaStream_t s) {
+// One host-side source of ciphertexts: `count` rows of int64 (A, b).
+struct HostPart {
+    const int64_t* A;
+    const int64_t* b;
+    int64_t count;
+};
+
+// int64 host parts (stacked in order) -> device uint32 rows, through the
+// pinned slots.  Returns the first CUDA error.  The caller's arrays may be
+// reused when it returns (every slot was packed from them before the return).
+inline cudaError_t upload_parts(PinnedSlots& ps, const HostPart* parts, int nparts, int n, int stride,
+                                uint32_t qmask, uint32_t* d_rows, cudaStream_t s) {
     cudaError_t e = ps.ensure();
     if (e != cudaSuccess) return e;
     const int64_t chunk = std::max<int64_t>(1, (int64_t)(PinnedSlots::SLOT_BYTES / (4 * (size_t)stride)));
     int k = 0;
-    for (int64_t r0 = 0; r0 < count; r0 += chunk, k ^= 1) {
-        const int64_t r1 = std::min(count, r0 + chunk);
-        if ((e = cudaEventSynchronize(ps.ev[k])) != cudaSuccess) return e;  // slot's last DMA done
-        uint32_t* slot = static_cast<uint32_t*>(ps.slot[k]);
-        pack_rows_host(A, b, r0, r1, n, stride, qmask, slot);
-        if ((e = cudaMemcpyAsync(d_rows + r0 * stride, slot, (size_t)(r1 - r0) * stride * 4,
-                                 cudaMemcpyHostToDevice, s)) != cudaSuccess)
-            return e;
-        if ((e = cudaEventRecord(ps.ev[k], s)) != cudaSuccess) return e;
+    int64_t dst_row = 0;
+    for (int p = 0; p < nparts; ++p) {
+        const HostPart& hp = parts[p];
+        for (int64_t r0 = 0; r0 < hp.count; r0 += chunk, k = (k + 1) % PinnedSlots::NSLOT) {
+            const int64_t r1 = std::min(hp.count, r0 + chunk);
+            if ((e = cudaEventSynchronize(ps.ev[k])) != cudaSuccess) return e;  // slot's last DMA done
+            uint32_t* slot = static_cast<uint32_t*>(ps.slot[k]);
+            pack_rows_host(hp.A, hp.b, r0, r1, n, stride, qmask, slot);
+            if ((e = cudaMemcpyAsync(d_rows + (dst_row + r0) * stride, slot, (size_t)(r1 - r0) * stride * 4,
+                                     cudaMemcpyHostToDevice, s)) != cudaSuccess)
+                return e;
+            if ((e = cudaEventRecord(ps.ev[k], s)) != cudaSuccess) return e;
+        }
+        dst_row += hp.count;
     }
     return cudaSuccess;
+}
+
+inline cudaError_t upload_rows(PinnedSlots& ps, const int64_t* A, const int64_t* b, int64_t count, int n,
+                               int stride, uint32_t qmask, uint32_t* d_rows, cudaStream_t s) {
+    const HostPart part{A, b, count};
+    return upload_parts(ps, &part, 1, n, stride, qmask, d_rows, s);
 }
 
 // device uint32 rows -> int64 host (A, b); returns after the host arrays are
@@ -205,10 +229,11 @@ inline cudaError_t download_rows(PinnedSlots& ps, const uint32_t* d_rows, int64_
                                  int64_t* A, int64_t* b, cudaStream_t s) {
     cudaError_t e = ps.ensure();
     if (e != cudaSuccess) return e;
+    constexpr int NS = PinnedSlots::NSLOT;
     const int64_t chunk = std::max<int64_t>(1, (int64_t)(PinnedSlots::SLOT_BYTES / (4 * (size_t)stride)));
     const int64_t nchunks = (count + chunk - 1) / chunk;
     auto issue = [&](int64_t c) -> cudaError_t {
-        const int k = (int)(c & 1);
+        const int k = (int)(c % NS);
         const int64_t r0 = c * chunk, r1 = std::min(count, r0 + chunk);
         cudaError_t e2 = cudaEventSynchronize(ps.ev[k]);
         if (e2 != cudaSuccess) return e2;
@@ -217,12 +242,13 @@ inline cudaError_t download_rows(PinnedSlots& ps, const uint32_t* d_rows, int64_
         if (e2 != cudaSuccess) return e2;
         return cudaEventRecord(ps.ev[k], s);
     };
-    if ((e = issue(0)) != cudaSuccess) return e;
+    // keep NS-1 chunks in flight ahead of the one being unpacked
+    for (int64_t c = 0; c < std::min<int64_t>(nchunks, NS - 1); ++c)
+        if ((e = issue(c)) != cudaSuccess) return e;
     for (int64_t c = 0; c < nchunks; ++c) {
-        const int k = (int)(c & 1);
+        const int k = (int)(c % NS);
         if ((e = cudaEventSynchronize(ps.ev[k])) != cudaSuccess) return e;
-        // the next chunk's DMA runs while this one is unpacked
-        if (c + 1 < nchunks && (e = issue(c + 1)) != cudaSuccess) return e;
+        if (c + NS - 1 < nchunks && (e = issue(c + NS - 1)) != cudaSuccess) return e;
         const int64_t r0 = c * chunk, r1 = std::min(count, r0 + chunk);
         unpack_rows_host(static_cast<const uint32_t*>(ps.slot[k]), r0, r1, n, stride, A, b);
     }

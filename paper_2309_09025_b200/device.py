@@ -184,11 +184,35 @@ class DeviceContext:
         t.zero_()
         return t
 
-    def rows_from_host(self, A, b):
+    def rows_from_host(self, A, b, out=None):
+        """int64 host (A, b) -> device rows (a new tensor, or the rows of `out`)."""
         A, b = _i64(A), _i64(b)
-        rows = self.empty_rows(len(b))
+        if A.ndim != 2 or A.shape != (len(b), self.params.n):
+            raise ParameterError("ciphertext arrays do not match params")
+        rows = self.empty_rows(len(b)) if out is None else out
+        if rows.shape[0] != len(b):
+            raise ParameterError("output rows do not match the ciphertext count")
         _lib.check(self.lib.fdsnn_rows_from_host(self.h, _ptr(A), _ptr(b), len(b),
                                                  _tptr(rows), self._stream()))
+        return rows
+
+    def rows_from_host_parts(self, parts, out=None):
+        """[(A, b), ...] int64 host arrays -> device rows stacked in order."""
+        arrs = []
+        for A, b in parts:
+            A, b = _i64(A), _i64(b)
+            if A.ndim != 2 or A.shape != (len(b), self.params.n):
+                raise ParameterError("ciphertext arrays do not match params")
+            arrs.append((A, b))
+        total = sum(len(b) for _, b in arrs)
+        rows = self.empty_rows(total) if out is None else out
+        if rows.shape[0] != total:
+            raise ParameterError("output rows do not match the ciphertext count")
+        k = len(arrs)
+        pa = (ctypes.c_void_p * k)(*[a.ctypes.data for a, _ in arrs])
+        pb = (ctypes.c_void_p * k)(*[b.ctypes.data for _, b in arrs])
+        cnt = (ctypes.c_int64 * k)(*[len(b) for _, b in arrs])
+        _lib.check(self.lib.fdsnn_rows_from_host_parts(self.h, k, pa, pb, cnt, _tptr(rows), self._stream()))
         return rows
 
     def rows_to_host(self, rows):

@@ -160,8 +160,7 @@ def _plain_case(tag, prm):
     import paper_2309_09025_b200 as api
     lif = W.lif_for(api, prm)
     net = (W.config2_network if tag == "c2" else W.config4_network)(api, lif)
-    nimg = 32 if tag == "c2" else 4
-    imgs = W.synth_images(nimg)
+    imgs = W.synth_images(32)
     return net, imgs, W.layers_for_oracle(net)
 
 
@@ -181,6 +180,25 @@ def test_oracle_plain_infer_golden(tag, desk, c4prm):
             assert np.array_equal(c, g[f"{tag}_counts{li}"][k]), (k, li)
         overflowing += over > 0
     assert overflowing == int(g[f"{tag}_overflow_images"][0])
+
+
+@pytest.mark.parametrize("tag", ["c2", "c4"])
+def test_oracle_twin_matches_reference_encrypted_run(tag, desk, c4prm):
+    """The mod-p twin (the checker for every full-batch GPU test) equals the
+    reference's ENCRYPTED infer (network.py:459-491) on image 0 of configs 2
+    and 4: every spiking layer's decrypted spikes at every timestep and the
+    decrypted scores (config2_img0.npz / config4_img0.npz)."""
+    name = "config2_img0" if tag == "c2" else "config4_img0"
+    path = os.path.join(GOLDEN, name + ".npz")
+    g = np.load(path)
+    prm = desk if tag == "c2" else c4prm
+    net, imgs, layers = _plain_case(tag, prm)
+    x = (imgs[0].astype(np.float64) / 255.0 >= 0.5).astype(np.int64).ravel()
+    score, log = O.twin_infer(x, layers, net.T, prm.p)
+    assert np.array_equal(score, g["scores"])
+    assert len(log) == sum(1 for k in g.files if k.startswith("l"))
+    for li, t, v in log:
+        assert np.array_equal(v, g[f"l{li}_t{t}"]), (li, t)
 
 
 # ---------------------------------------------------- algebra layer (ring.npz)
