@@ -21,6 +21,7 @@
 #include "ks_umma.cuh"
 #include "linear.cuh"
 #include "pbs.cuh"
+#include "pbs_cluster.cuh"
 #include "plain.cuh"
 #include "lwe_dev.cuh"
 #include "ring_ops.cuh"
@@ -106,6 +107,9 @@ struct fdsnn_ctx {
     struct StreamScratch { Buf ext, ks_dig, stage; PinnedSlots pin; };
     std::map<cudaStream_t, StreamScratch> scratch;
     int64_t wide_max = 148;  // largest batch routed to the latency kernel (FDSNN_WIDE_MAX)
+    // CTA-pair kernel (pbs_cluster.cuh): one rotation per SM pair up to
+    // cluster_g1_max, two up to cluster_max (FDSNN_CLUSTER_G1_MAX / _MAX)
+    int64_t cluster_g1_max = 74, cluster_max = 148;
     int64_t sm_count = 148;
     bool keys_loaded = false;  // bootstrapping key (and its key-switch key)
     bool ks_loaded = false;    // key-switch key
@@ -181,6 +185,33 @@ int launch_br_wide_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_t s
     return FDSNN_OK;
 }
 
+template <int G, bool RAW, bool MARGIN>
+int launch_br_cluster_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_t s) {
+    const size_t smem = pbsc_smem_bytes<512, 2>(G, ctx->dp.n);
+    auto kern = pbs_blind_rotate_cluster_kernel<512, 2, G, RAW, MARGIN>;
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t pairs = (V + G - 1) / G;
+    kern<<<(unsigned)(2 * pairs), G * PBSC_T, smem, s>>>(a);
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+
+// Latency regime (DESK-shaped rings): one rotation (G = 1) or two (G = 2)
+// per SM pair.
+int launch_br_cluster(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_t s) {
+    const bool g2 = V > ctx->cluster_g1_max;
+    if (raw) {
+        if (g2) return ctx->track_margin ? launch_br_cluster_t<2, true, true>(ctx, a, V, s)
+                                         : launch_br_cluster_t<2, true, false>(ctx, a, V, s);
+        return ctx->track_margin ? launch_br_cluster_t<1, true, true>(ctx, a, V, s)
+                                 : launch_br_cluster_t<1, true, false>(ctx, a, V, s);
+    }
+    if (g2) return ctx->track_margin ? launch_br_cluster_t<2, false, true>(ctx, a, V, s)
+                                     : launch_br_cluster_t<2, false, false>(ctx, a, V, s);
+    return ctx->track_margin ? launch_br_cluster_t<1, false, true>(ctx, a, V, s)
+                             : launch_br_cluster_t<1, false, false>(ctx, a, V, s);
+}
+
 int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_t s) {
     if (V <= 0) return FDSNN_OK;
     TimerScope ts(ctx, 0, s);
@@ -206,6 +237,7 @@ int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_
                 if (rem == 0) return FDSNN_OK;
                 PbsArgs t = a;
                 t.v_base = a.v_base + full;
+                if (rem <= ctx->cluster_max) return launch_br_cluster(ctx, t, rem, raw, s);
                 if (rem <= ctx->wide_max) {  // latency regime: one CTA per rotation, digits in parallel
                     if (raw) return ctx->track_margin ? launch_br_wide_t<true, true>(ctx, t, rem, s)
                                                       : launch_br_wide_t<true, false>(ctx, t, rem, s);
@@ -509,6 +541,10 @@ int fdsnn_ctx_create(const fdsnn_params* prm, int32_t device, fdsnn_ctx** out) {
         ctx->wide_max = dprop.multiProcessorCount;
         ctx->sm_count = dprop.multiProcessorCount;
         if (const char* e = getenv("FDSNN_WIDE_MAX")) ctx->wide_max = atoll(e);
+        ctx->cluster_g1_max = dprop.multiProcessorCount / 2;
+        ctx->cluster_max = dprop.multiProcessorCount;
+        if (const char* e = getenv("FDSNN_CLUSTER_G1_MAX")) ctx->cluster_g1_max = atoll(e);
+        if (const char* e = getenv("FDSNN_CLUSTER_MAX")) ctx->cluster_max = atoll(e);
         DevParams& d = ctx->dp;
         d.n = p.n;
         d.N = p.N;

@@ -172,7 +172,11 @@ constexpr uint32_t PBS_TMEM_OWN = 128;
 // frequency accumulators wait in TMEM (columns 256 + 64*(w/4)) while the
 // second polynomial is transformed.
 template <int M, int G, bool MODE_RAW, bool TRACK_MARGIN, bool PAIR = false, int LQ = 2>
+#ifdef FDSNN_MAXNREG
+__global__ void __maxnreg__(FDSNN_MAXNREG)
+#else
 __global__ void __launch_bounds__(G * (M / 8), 1)
+#endif
 pbs_blind_rotate_kernel(const PbsArgs args) {
     constexpr uint32_t TMEM_COLS = PAIR ? 512 : PBS_TMEM_COLS;
     constexpr int NA = 2 * M;  // words per accumulator poly

@@ -286,3 +286,26 @@ def test_host_boundary_concurrent_streams(desk, desk_keys):
         t.join()
     assert not errs, errs
     assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+@pytest.mark.parametrize("count", [1, 2, 37, 74, 75, 111, 148])
+def test_cluster_latency_regime(desk, desk_keys, count):
+    """Batches up to the SM count run on the CTA-pair kernel (one rotation per
+    SM pair up to 74, two per pair above): bootstraps (with key switch) and
+    raw-mode rotations bit-exact against the oracle, first/middle/last."""
+    sk, _, bsk = desk_keys
+    rng = np.random.default_rng(70 + count)
+    A, b = lwe.encrypt_batch(rng.integers(-511, 513, count), sk, desk, rng)
+    g = neuron.g_fire(desk.p)
+    oA, ob = bootstrap.bootstrap_batch(g, A, b, bsk)
+    key = oracle_key(desk, bsk)
+    idx = sorted({0, count // 2, count - 1})
+    wA, wb = O.bootstrap_batch(g.table, A[idx], b[idx], key)
+    assert np.array_equal(oA[idx], wA) and np.array_equal(ob[idx], wb)
+    acc = rng.integers(0, desk.q, (count, 2, desk.N))
+    a2N = rng.integers(0, 2 * desk.N, (count, desk.n))
+    a2N[:, 1::7] = 0  # identity steps inside the chain
+    orig = acc.copy()
+    got = bootstrap.blind_rotate_batch(acc, a2N, bsk)
+    for j in idx:
+        assert np.array_equal(got[j:j + 1], O.blind_rotate(orig[j:j + 1], a2N[j:j + 1], key)), j
