@@ -1286,6 +1286,18 @@ int fdsnn_probe_fp64_peak(fdsnn_ctx* ctx, double* tflops) {
     });
 }
 
+#ifdef FDSNN_PHASE_PROF
+// development build only (not part of the ABI): per-phase cycle sums of the
+// CTA-pair kernel, thread 0 of cluster 0
+int fdsnn_debug_phase_read(unsigned long long* out8) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out8, g_pbsc_phase, 8 * sizeof(unsigned long long));
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_pbsc_phase, z, sizeof z);
+    return FDSNN_OK;
+}
+#endif
+
 int fdsnn_flush_l2(fdsnn_ctx* ctx, void* stream) {
     return guarded([&]() -> int {
         if (!ctx) return set_err(FDSNN_ERR_STATE, "null context");

@@ -222,6 +222,35 @@ struct TwiddlesInTmem {
     }
 };
 
+// Twiddles read from the (L1-resident) global table: issue<PASS> starts the
+// loads before the exchange stores, finish<PASS> consumes them after the
+// barrier, so their latency hides behind the exchange; no registers are held
+// between passes.
+template <int M>
+struct TwiddlesFromGlobal {
+    const double2* tab;  // interior-pass table (twiddle_offset layout)
+    int t;
+    template <int PASS>
+    FDSNN_DEV void issue(uint32_t (&raw)[32]) const {
+        constexpr int R = PassInfo<M, PASS>::R;
+        constexpr int ns = PassInfo<M, PASS>::NS;
+        const double2* base = tab + twiddle_offset<M>(PASS);
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+            const double2 w = __ldg(base + (r - 1) * ns + (t % ns));
+            raw[4 * (r - 1)] = (uint32_t)__double2loint(w.x);
+            raw[4 * (r - 1) + 1] = (uint32_t)__double2hiint(w.x);
+            raw[4 * (r - 1) + 2] = (uint32_t)__double2loint(w.y);
+            raw[4 * (r - 1) + 3] = (uint32_t)__double2hiint(w.y);
+        }
+    }
+    template <int PASS>
+    FDSNN_DEV void finish(uint32_t (&raw)[32], double2 (&w)[8]) const {
+#pragma unroll
+        for (int r = 0; r < 7; ++r) w[r] = words_c(raw, r);
+    }
+};
+
 // One Stockham pass.  v holds 8/R independent R-point groups.
 template <int M, int PASS, bool INV>
 FDSNN_DEV void pass_body(double2 (&v)[8], const double2 (&w)[8]) {

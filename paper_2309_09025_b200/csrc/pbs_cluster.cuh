@@ -44,6 +44,22 @@ FDSNN_DEV void st_async_c(uint32_t raddr, double2 v, uint32_t rbar) {
                  ::"r"(raddr), "d"(v.x), "d"(v.y), "r"(rbar) : "memory");
 }
 
+#ifdef FDSNN_PHASE_PROF
+__device__ unsigned long long g_pbsc_phase[8];
+#define PHASE(k)                                                                  \
+    do {                                                                          \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                \
+            const long long now_ = clock64();                                     \
+            atomicAdd(&g_pbsc_phase[k], (unsigned long long)(now_ - ph_t0));      \
+            ph_t0 = now_;                                                         \
+        }                                                                         \
+    } while (0)
+#else
+#define PHASE(k) \
+    do {         \
+    } while (0)
+#endif
+
 constexpr int PBSC_T = 64;  // threads per rotation per CTA (M = 512: 8 points each)
 
 template <int M>
@@ -86,6 +102,11 @@ pbs_blind_rotate_cluster_kernel(const PbsArgs args) {
     int32_t* acc = reinterpret_cast<int32_t*>(recv + 2 * M);
     uint16_t* a2N = reinterpret_cast<uint16_t*>(acc + N);
 
+    auto a2N_of = [&](int gg) {
+        unsigned char* base = smem_raw + 128 + S * CHUNK + (size_t)gg * pbsc_group_bytes<M>(n);
+        return reinterpret_cast<const uint16_t*>(base + 2 * PADM * sizeof(double2) + 2 * M * sizeof(double2) +
+                                                 (size_t)N * sizeof(int32_t));
+    };
     const uint32_t cr = cluster_ctarank();  // polynomial owned by this CTA
     const uint32_t partner = cr ^ 1u;
     const int64_t V = (int64_t)args.nlut * args.count;
@@ -174,6 +195,9 @@ pbs_blind_rotate_cluster_kernel(const PbsArgs args) {
     // partner's receive buffers and mbarriers for this rotation
     const uint32_t r_recv = mapa_shared(recv, partner);
     const uint32_t r_bar = mapa_shared(&xfull[2 * g], partner);
+#ifdef FDSNN_PHASE_PROF
+    long long ph_t0 = clock64();
+#endif
 
     for (int i = 0; i < n; ++i) {
         const int k = active ? (int)a2N[i] : 0;
@@ -192,19 +216,21 @@ pbs_blind_rotate_cluster_kernel(const PbsArgs args) {
                 v1[r] = make_double2((double)(((y0 >> bg) & bmask) - halfB1),
                                      (double)(((y1 >> bg) & bmask) - halfB1));
             }
+            PHASE(0);
             // ---- 2. both levels' forward transforms (twist fused into pass 0);
             // the key chunks are waited for before the last pass
             const int s0 = (i & 1) * L, s1 = s0 + 1;
             const uint32_t kpar = (uint32_t)((i >> 1) & 1);
+            const double2* k0 = ring + (size_t)s0 * 2 * M;
+            const double2* k1 = ring + (size_t)s1 * 2 * M;
             auto keys_ready = [&]() {
                 mbar_wait(&full[s0], kpar);
                 mbar_wait(&full[s1], kpar);
             };
             fft_group2<M, false, TwiddlesInRegs<M>, decltype(keys_ready), true, true>(v0, v1, t, tw, buf0, buf1, gs,
                                                                                     keys_ready, twist);
+            PHASE(1);
             // ---- 3. MAC: this CTA's two digit rows into both output polys
-            const double2* k0 = ring + (size_t)s0 * 2 * M;
-            const double2* k1 = ring + (size_t)s1 * 2 * M;
             const int xp = xn & 1;
             const uint32_t xpar = (uint32_t)((xn >> 1) & 1);
             double2 O[8];
@@ -221,15 +247,19 @@ pbs_blind_rotate_cluster_kernel(const PbsArgs args) {
                            r_bar + (uint32_t)(xp * sizeof(uint64_t)));
                 O[r] = po;
             }
+            PHASE(2);
             // ---- 5. own sum, inverse transform, untwist, round, add
             mbar_wait(&xfull[2 * g + xp], xpar);
+            PHASE(3);
 #pragma unroll
             for (int r = 0; r < 8; ++r) O[r] = cadd(O[r], recv[xp * M + t + r * T]);
             gs.sync();  // every thread of the rotation has read recv[xp]
             if (t == 0) mbar_arrive_expect_tx(&xfull[2 * g + xp], XBYTES);  // re-arm for exchange xn + 2
             ++xn;
             int ex = 0;
+            PHASE(4);
             fft_group<M, true>(O, t, tw, buf0, buf1, ex, gs);
+            PHASE(5);
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
                 const int p = t + r * T;
@@ -243,16 +273,24 @@ pbs_blind_rotate_cluster_kernel(const PbsArgs args) {
                 acc[p + M] = (int32_t)(((uint32_t)acc[p + M] + (uint32_t)e1) & qmask);
             }
         }
+        PHASE(6);
         __syncthreads();  // accumulators updated; every reader of this step's key stages done
         if (threadIdx.x == 0 && i + 2 < n) {
+            // a stage some rotation consumed this step has landed already;
+            // otherwise (all identity steps) wait for the copy before re-arming
+            bool consumed = false;
+            for (int gg = 0; gg < G; ++gg)
+                consumed |= (args.v_base + (int64_t)(blockIdx.x >> 1) * G + gg < V) &&
+                            a2N_of(gg)[i] != 0;
             for (int l = 0; l < L; ++l) {
                 const int s = (i & 1) * L + l;
-                mbar_wait(&full[s], (uint32_t)((i >> 1) & 1));  // this step's copy landed (even if unused)
+                if (!consumed) mbar_wait(&full[s], (uint32_t)((i >> 1) & 1));
                 mbar_arrive_expect_tx(&full[s], CHUNK);
                 bulk_g2s(ring + (size_t)s * 2 * M, args.bsk + chunk_of(i + 2, l) * 2 * M, CHUNK, &full[s]);
             }
         }
     }
+    PHASE(7);
     (void)nsteps_chunks;
     if constexpr (TRACK_MARGIN) {
         if (args.margin && active) atomicMax(args.margin, (unsigned long long)__double_as_longlong(err_max));
