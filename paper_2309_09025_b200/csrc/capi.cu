@@ -1064,13 +1064,26 @@ int operator_apply_impl(fdsnn_ctx* ctx, int32_t op_id, const uint32_t* d_in, int
     const DevParams& d = ctx->dp;
     TimerScope ts(ctx, 2, s);
     if (op.dense) {
-        const int64_t big = (int64_t)((op.out_cells + LIN_ROWS - 1) / LIN_ROWS) * ((d.stride + LIN_COLS - 1) / LIN_COLS) * batch;
+        // full 128-column tiles on the tiled kernel; a tail of at most one
+        // 16-byte column group (DESK: b + 3 pad words after 512 mask columns)
+        // as warp dot products instead of a nearly empty tile
+        const int full_tiles = d.stride / LIN_COLS;
+        const bool tail4 = d.stride - full_tiles * LIN_COLS == 4;
+        const int ctiles = tail4 ? full_tiles : (d.stride + LIN_COLS - 1) / LIN_COLS;
+        const int64_t big = (int64_t)((op.out_cells + LIN_ROWS - 1) / LIN_ROWS) * ctiles * batch;
         if (big < 2 * 148) {  // small operator: half-height tiles, twice the CTAs
-            dim3 grid((op.out_cells + 31) / 32, (d.stride + LIN_COLS - 1) / LIN_COLS, (unsigned)batch);
+            dim3 grid((op.out_cells + 31) / 32, ctiles, (unsigned)batch);
             linear_dense_kernel<4><<<grid, 256, 0, s>>>(op.w, op.out_cells, op.in_cells, d_in, d_out, d.stride, d.qmask);
         } else {
-            dim3 grid((op.out_cells + LIN_ROWS - 1) / LIN_ROWS, (d.stride + LIN_COLS - 1) / LIN_COLS, (unsigned)batch);
+            dim3 grid((op.out_cells + LIN_ROWS - 1) / LIN_ROWS, ctiles, (unsigned)batch);
             linear_dense_kernel<8><<<grid, 256, 0, s>>>(op.w, op.out_cells, op.in_cells, d_in, d_out, d.stride, d.qmask);
+        }
+        if (tail4) {
+            CU(cudaGetLastError());
+            ts.kernels = 2;
+            const int64_t warps = (int64_t)batch * op.out_cells;
+            linear_tail_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
+                op.w, op.out_cells, op.in_cells, d_in, d_out, d.stride, full_tiles * LIN_COLS, d.qmask, (int)batch);
         }
     } else {
         dim3 grid(op.out_cells, (unsigned)batch);

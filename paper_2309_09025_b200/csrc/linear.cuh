@@ -28,8 +28,10 @@ linear_dense_kernel(const int32_t* __restrict__ Wm, int out_cells, int in_cells,
                     const uint32_t* __restrict__ X, uint32_t* __restrict__ Y,
                     int stride, uint32_t qmask) {
     constexpr int TR = 8 * RPT;
-    __shared__ __align__(16) int32_t ws[LIN_K][TR];
-    __shared__ __align__(16) uint32_t xs[LIN_K][LIN_COLS];
+    constexpr int WE = (LIN_K * TR + 255) / 256;            // weight elements per thread per stage
+    constexpr int XE = (LIN_K * (LIN_COLS / 4) + 255) / 256;  // 16-byte ciphertext vectors per thread
+    __shared__ __align__(16) int32_t ws[2][LIN_K][TR];
+    __shared__ __align__(16) uint32_t xs[2][LIN_K][LIN_COLS];
     const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
     const int r0 = blockIdx.x * TR;
     const int c0 = blockIdx.y * LIN_COLS;
@@ -41,36 +43,65 @@ linear_dense_kernel(const int32_t* __restrict__ Wm, int out_cells, int in_cells,
     for (int a = 0; a < RPT; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0u;
-    for (int k0 = 0; k0 < in_cells; k0 += LIN_K) {
-        for (int e = threadIdx.x; e < LIN_K * TR; e += blockDim.x) {
+    // stage k0's tiles are fetched into registers one stage ahead (the global
+    // latency hides behind the current stage's multiply-adds), then stored
+    // into the other shared-memory buffer
+    int32_t wreg[WE];
+    uint4 xreg[XE];
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int u = 0; u < WE; ++u) {
+            const int e = threadIdx.x + u * 256;
             const int rr = e / LIN_K, kk = e % LIN_K;
             const int r = r0 + rr, k = k0 + kk;
-            ws[kk][rr] = (r < out_cells && k < in_cells) ? Wm[(size_t)r * in_cells + k] : 0;
+            wreg[u] = (e < LIN_K * TR && r < out_cells && k < in_cells) ? __ldg(Wm + (size_t)r * in_cells + k) : 0;
         }
-        for (int e = threadIdx.x; e < LIN_K * (LIN_COLS / 4); e += blockDim.x) {
+#pragma unroll
+        for (int u = 0; u < XE; ++u) {
+            const int e = threadIdx.x + u * 256;
             const int kk = e / (LIN_COLS / 4), cc = (e % (LIN_COLS / 4)) * 4;
             const int k = k0 + kk, c = c0 + cc;
-            uint4 val = make_uint4(0, 0, 0, 0);
-            if (k < in_cells && c < stride)
-                val = *reinterpret_cast<const uint4*>(Xb + (size_t)k * stride + c);
-            *reinterpret_cast<uint4*>(&xs[kk][cc]) = val;
+            xreg[u] = (e < LIN_K * (LIN_COLS / 4) && k < in_cells && c < stride)
+                          ? __ldg(reinterpret_cast<const uint4*>(Xb + (size_t)k * stride + c))
+                          : make_uint4(0, 0, 0, 0);
         }
-        __syncthreads();
+    };
+    auto put = [&](int buf) {
+#pragma unroll
+        for (int u = 0; u < WE; ++u) {
+            const int e = threadIdx.x + u * 256;
+            if (e < LIN_K * TR) ws[buf][e % LIN_K][e / LIN_K] = wreg[u];
+        }
+#pragma unroll
+        for (int u = 0; u < XE; ++u) {
+            const int e = threadIdx.x + u * 256;
+            if (e < LIN_K * (LIN_COLS / 4))
+                *reinterpret_cast<uint4*>(&xs[buf][e / (LIN_COLS / 4)][(e % (LIN_COLS / 4)) * 4]) = xreg[u];
+        }
+    };
+    fetch(0);
+    put(0);
+    __syncthreads();
+    int buf = 0;
+    for (int k0 = 0; k0 < in_cells; k0 += LIN_K, buf ^= 1) {
+        const bool more = k0 + LIN_K < in_cells;
+        if (more) fetch(k0 + LIN_K);
 #pragma unroll
         for (int kk = 0; kk < LIN_K; ++kk) {
             int32_t wd[RPT];
 #pragma unroll
             for (int a = 0; a < RPT; a += 4) {
-                const int4 w4 = *reinterpret_cast<const int4*>(&ws[kk][ty * RPT + a]);
+                const int4 w4 = *reinterpret_cast<const int4*>(&ws[buf][kk][ty * RPT + a]);
                 wd[a] = w4.x; wd[a + 1] = w4.y; wd[a + 2] = w4.z; wd[a + 3] = w4.w;
             }
-            const uint4 xv = *reinterpret_cast<const uint4*>(&xs[kk][tx * 4]);
+            const uint4 xv = *reinterpret_cast<const uint4*>(&xs[buf][kk][tx * 4]);
             const uint32_t xd[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
             for (int a = 0; a < RPT; ++a)
 #pragma unroll
                 for (int b = 0; b < 4; ++b) acc[a][b] += (uint32_t)wd[a] * xd[b];
         }
+        if (more) put(buf ^ 1);  // the other buffer's last readers passed the previous barrier
         __syncthreads();
     }
 #pragma unroll
@@ -84,6 +115,38 @@ linear_dense_kernel(const int32_t* __restrict__ Wm, int out_cells, int in_cells,
             *reinterpret_cast<uint4*>(Yb + (size_t)r * stride + c) = o;
         }
     }
+}
+
+// The last few columns of the rows ([c0, stride): the body b and the row
+// padding when n is a multiple of the 128-column tile) as warp dot products,
+// so the dense kernel's grid covers only full column tiles.  One warp per
+// (batch, output row); each lane sums a strided slice of the input rows for
+// up to 4 columns, then the warp reduces.
+__global__ void __launch_bounds__(256)
+linear_tail_kernel(const int32_t* __restrict__ Wm, int out_cells, int in_cells, const uint32_t* __restrict__ X,
+                   uint32_t* __restrict__ Y, int stride, int c0, uint32_t qmask, int batch) {
+    const int lane = threadIdx.x % 32;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    if (wid >= (int64_t)batch * out_cells) return;
+    const int bidx = (int)(wid / out_cells), r = (int)(wid % out_cells);
+    const uint32_t* Xb = X + (size_t)bidx * in_cells * stride + c0;
+    const int32_t* w = Wm + (size_t)r * in_cells;
+    uint32_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    for (int k = lane; k < in_cells; k += 32) {
+        const uint32_t wk = (uint32_t)__ldg(w + k);
+        const uint4 xv = __ldg(reinterpret_cast<const uint4*>(Xb + (size_t)k * stride));
+        s0 += wk * xv.x; s1 += wk * xv.y; s2 += wk * xv.z; s3 += wk * xv.w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+    }
+    if (lane == 0)
+        *reinterpret_cast<uint4*>(Y + ((size_t)bidx * out_cells + r) * stride + c0) =
+            make_uint4(s0 & qmask, s1 & qmask, s2 & qmask, s3 & qmask);
 }
 
 // CSR: row_ptr (out+1), col_idx/val (nnz).  grid = (out_cells, batch).
