@@ -378,7 +378,10 @@ def run_b200(args, world, rank, local):
 
     # ---- roofline of the dominant kernel (blind rotation)
     peak = dev.fp64_peak_tflops()
-    br_launch_ms = br_ms / max(br_n, 1)
+    # one blind-rotation call per fused LIF call (T_STEPS per step); a call
+    # may be served by more than one kernel launch (br_n counts launches)
+    br_calls = T_STEPS * args.steps
+    br_launch_ms = br_ms / max(br_calls, 1)
     pbs_per_launch = BATCH * NEURONS * 2
     achieved = FLOPS_PER_PBS_DESK * pbs_per_launch / (br_launch_ms * 1e-3) / 1e12
     traffic, pipe_active = None, None
@@ -407,7 +410,10 @@ def run_b200(args, world, rank, local):
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "fp64_pipe_active": pipe_active,
-                     "kernel": "pbs_blind_rotate_kernel<512,4>",
+                     "kernel": "blind rotation per fused LIF call (4096 PBS): pbs_br16_kernel, 3 waves of 8 "
+                               "rotations per SM (3552) + pbs_blind_rotate_kernel<512,4,..> for the 544-rotation "
+                               "remainder (4 per SM); achieved = flops of the call / the call's device time",
+                     "br_kernel_launches_per_call": br_n / max(br_calls, 1),
                      "flops_per_pbs": FLOPS_PER_PBS_DESK, "pbs_per_launch": pbs_per_launch,
                      "peak_source": "DFMA loop measured live in this run (fdsnn_probe_fp64_peak); "
                                     "MEASURED_PEAKS.json has no FP64 entry"},

@@ -22,6 +22,7 @@
 #include "linear.cuh"
 #include "pbs.cuh"
 #include "pbs_cluster.cuh"
+#include "pbs16.cuh"
 #include "plain.cuh"
 #include "lwe_dev.cuh"
 #include "ring_ops.cuh"
@@ -95,6 +96,10 @@ struct fdsnn_ctx {
     cudaStream_t stream = nullptr;
     double2* tables = nullptr;  // W | twist | untw
     double2* bsk = nullptr;
+    // M = 512: the warp-per-rotation kernel's key layout and lane table (pbs16.cuh)
+    double2* bsk16 = nullptr;
+    double2* tab16 = nullptr;
+    bool br16 = true;  // FDSNN_BR16=0 selects the 4-rotations-per-CTA kernel
     uint32_t* ksk = nullptr;
     uint32_t* kskb = nullptr;  // body column of the KSK, contiguous
     // tensor-core key switch (ks_umma.cuh): limb tiles of the KSK
@@ -196,6 +201,26 @@ int launch_br_cluster_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, cudaStream_
     return FDSNN_OK;
 }
 
+template <bool RAW, bool MARGIN>
+int launch_br16_t(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, int G, cudaStream_t s) {
+    auto kern = pbs_br16_kernel<RAW, MARGIN>;
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)br16_smem_bytes(BR16_MAXW, ctx->dp.n)));
+    const int64_t blocks = (V + G - 1) / G;
+    kern<<<(unsigned)blocks, 32 * G, br16_smem_bytes(G, ctx->dp.n), s>>>(a);
+    CU(cudaGetLastError());
+    return FDSNN_OK;
+}
+int launch_br16(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, int G, bool raw, cudaStream_t s) {
+    PbsArgs b = a;
+    b.bsk16 = ctx->bsk16;
+    b.tab16 = ctx->tab16;
+    if (raw) return ctx->track_margin ? launch_br16_t<true, true>(ctx, b, V, G, s)
+                                      : launch_br16_t<true, false>(ctx, b, V, G, s);
+    return ctx->track_margin ? launch_br16_t<false, true>(ctx, b, V, G, s)
+                             : launch_br16_t<false, false>(ctx, b, V, G, s);
+}
+
 // Latency regime (DESK-shaped rings): one rotation (G = 1) or two (G = 2)
 // per SM pair.
 int launch_br_cluster(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_t s) {
@@ -223,20 +248,44 @@ int launch_br(fdsnn_ctx* ctx, const PbsArgs& a, int64_t V, bool raw, cudaStream_
             // (G=1 CTAs are small enough for 2 per SM: <= 296 rotations fit in one wave)
             // gadget levels L == 2 (DESK): the paired-level transform variant
             if (ctx->dp.L == 2) {
-                // Rounds of 4 rotations per SM, then the remainder at the
-                // density that finishes it fastest: 1/SM on the latency
-                // kernel, 2 or 3 per SM, or folded into the 4/SM launch.
-                const int64_t sms = ctx->sm_count, round4 = 4 * sms;
-                int64_t rem = V % round4, full = V - rem;
-                if (rem > 3 * sms) { full = V; rem = 0; }
-                ts.kernels = (full > 0) + (rem > 0);
+                // Large batches: waves of 8 rotations per SM on the
+                // warp-per-rotation kernel (pbs16.cuh, highest throughput;
+                // one launch, its last CTA possibly partial).
+                // What is left (and any batch below one such wave, where one
+                // warp per rotation would mean a full rotation latency for a
+                // fraction of the work) runs on the 64-thread-transform
+                // kernels: rounds of 4 rotations per SM, then the remainder
+                // at the density that finishes it fastest -- SM pairs
+                // (pbs_cluster.cuh), 2 or 3 per SM, or folded into the 4/SM
+                // launch.
+                const int64_t sms = ctx->sm_count;
+                PbsArgs t = a;
+                int64_t W = V;
+                int nk = 0;
+                if (ctx->br16 && ctx->bsk16) {
+                    // a remainder above 3/4 of a wave finishes soonest as a
+                    // partial wave of the same launch
+                    const int64_t wave = (int64_t)BR16_MAXW * sms;
+                    int64_t full16 = V / wave * wave;
+                    if (V - full16 > 6 * sms) full16 = V;
+                    if (full16 > 0) {
+                        int rc = launch_br16(ctx, a, full16, BR16_MAXW, raw, s);
+                        if (rc) return rc;
+                        ++nk;
+                    }
+                    t.v_base += full16;
+                    W -= full16;
+                }
+                const int64_t round4 = 4 * sms;
+                int64_t rem = W % round4, full = W - rem;
+                if (rem > 3 * sms) { full = W; rem = 0; }
+                ts.kernels = nk + (full > 0) + (rem > 0);
                 if (full > 0) {
-                    int rc = launch_br_m<512, 4, true>(ctx, a, full, raw, s);
+                    int rc = launch_br_m<512, 4, true>(ctx, t, full, raw, s);
                     if (rc) return rc;
                 }
                 if (rem == 0) return FDSNN_OK;
-                PbsArgs t = a;
-                t.v_base = a.v_base + full;
+                t.v_base += full;
                 if (rem <= ctx->cluster_max) return launch_br_cluster(ctx, t, rem, raw, s);
                 if (rem <= ctx->wide_max) {  // latency regime: one CTA per rotation, digits in parallel
                     if (raw) return ctx->track_margin ? launch_br_wide_t<true, true>(ctx, t, rem, s)
@@ -594,6 +643,16 @@ int fdsnn_ctx_create(const fdsnn_params* prm, int32_t device, fdsnn_ctx** out) {
                     tab.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
                 }
         }
+        if (const char* e = getenv("FDSNN_BR16")) ctx->br16 = atoi(e) != 0;
+        if (M == 512) {
+            std::vector<double2> t16(32 * r16::TAB);
+            r16::build_table(p.N, t16.data(), [](long double c, long double sn) { return make_double2((double)c, (double)sn); });
+            if (cudaMalloc(&ctx->tab16, t16.size() * sizeof(double2)) != cudaSuccess ||
+                cudaMemcpy(ctx->tab16, t16.data(), t16.size() * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess) {
+                fdsnn_ctx_destroy(ctx);
+                return set_err(FDSNN_ERR_CUDA, "device allocation failed");
+            }
+        }
         if (cudaMalloc(&ctx->tables, tab.size() * sizeof(double2)) != cudaSuccess ||
             cudaMemcpy(ctx->tables, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMalloc(&ctx->margin, sizeof(unsigned long long)) != cudaSuccess ||
@@ -615,6 +674,8 @@ int fdsnn_ctx_destroy(fdsnn_ctx* ctx) {
         for (auto* l : ctx->luts) cudaFree(l);
         for (auto& o : ctx->ops) { cudaFree(o.w); cudaFree(o.row_ptr); cudaFree(o.col_idx); cudaFree(o.val); }
         cudaFree(ctx->tables);
+        cudaFree(ctx->tab16);
+        cudaFree(ctx->bsk16);
         cudaFree(ctx->bsk);
         cudaFree(ctx->ksk);
         cudaFree(ctx->kskb);
@@ -670,6 +731,12 @@ int fdsnn_bsk_load(fdsnn_ctx* ctx, const int64_t* rows, const int64_t* ksk_A, co
                     break;
             }
             CU(cudaGetLastError());
+            if (M == 512) {  // the warp-per-rotation kernel's key (pbs16.cuh)
+                if (!ctx->bsk16) CU(cudaMalloc(&ctx->bsk16, (size_t)npoly * M * sizeof(double2)));
+                bsk_forward16_kernel<<<(unsigned)((npoly + 3) / 4), 128, 0, ctx->stream>>>(d_rows, npoly, d.log2q,
+                                                                                     ctx->tab16, ctx->bsk16);
+                CU(cudaGetLastError());
+            }
         }
         if (int rc = load_ksk_impl(ctx, ksk_A, ksk_b)) return rc;
         CU(cudaStreamSynchronize(ctx->stream));

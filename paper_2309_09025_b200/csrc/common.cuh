@@ -81,6 +81,11 @@ FDSNN_DEV long long round_product(double x) { return __double2ll_rn(x); }
 // Low 32 bits of the same rounding (the accumulator update is mod q <= 2^31).
 FDSNN_DEV uint32_t round_lo32(double x) { return (uint32_t)__double2ll_rn(x); }
 
+// Round-to-nearest-even of |x| < 2^51 on the FP64 pipe (no F2I): x + 1.5 2^52
+// lands in [2^52, 2^53) where the ulp is 1, so the sum's low mantissa word is
+// round(x) + 2^51 = round(x) mod 2^32.  Same integer as round_lo32.
+FDSNN_DEV uint32_t round_lo32_fp64(double x) { return (uint32_t)__double2loint(x + 6755399441055744.0); }
+
 FDSNN_DEV void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -191,6 +196,16 @@ FDSNN_DEV void tmem_wait16(uint32_t (&w)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;"
                  : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7]),
                    "+r"(w[8]), "+r"(w[9]), "+r"(w[10]), "+r"(w[11]), "+r"(w[12]), "+r"(w[13]), "+r"(w[14]), "+r"(w[15])
+                 :: "memory");
+}
+FDSNN_DEV void tmem_ld8_async(uint32_t taddr, uint32_t (&w)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                 : "r"(taddr) : "memory");
+}
+FDSNN_DEV void tmem_wait8(uint32_t (&w)[8]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7])
                  :: "memory");
 }
 // mark registers as completed by an earlier wait (no instruction emitted)

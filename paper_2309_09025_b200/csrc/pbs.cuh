@@ -63,6 +63,9 @@ struct PbsArgs {
     // output mode A: extracted z-LWE rows (virtual ct v at v*ext_stride)
     uint32_t* ext_out;
     unsigned long long* margin;  // optional max |x - round(x)| (as double bits)
+    // warp-per-rotation kernel (pbs16.cuh, M = 512): key in its layout, lane table
+    const double2* bsk16;
+    const double2* tab16;
 };
 
 template <int M>

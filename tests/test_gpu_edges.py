@@ -124,14 +124,17 @@ def test_fdsn_containers_to_device(toy, toy_keys, tmp_path):
         serial.load_bootstrap_key_device(tmp_path / "ct.bin", toy)
 
 
-@pytest.mark.parametrize("count", [148, 149, 296, 297, 445, 446, 447, 600, 740, 1040])
+@pytest.mark.parametrize("count", [148, 149, 296, 297, 445, 446, 447, 600, 740, 1040, 1100, 1184, 1185, 1333, 2303, 2668])
 def test_launch_regime_boundaries(desk, desk_keys, count):
-    """Batches either side of the launch-split points (full rounds of 4
-    rotations per SM, remainder on the latency kernel or at 2-3 per SM) give
-    oracle-identical outputs (first and last 6 checked).  445-447 end the
-    4-rotation launch with a CTA of 1, 2 and 3 active rotations: 3 is the
-    phase-skewed case with a single trailing group (which also refills the
-    key ring), 1-2 run unskewed."""
+    """Batches either side of the launch-split points give oracle-identical
+    outputs (first and last 6 checked): waves of 8 rotations per SM on the
+    warp-per-rotation kernel (1184 = one wave; 1185, 1333, 2668 add a
+    remainder; 1100 and 2303 end in a partial wave whose last CTA has 4 and 7
+    active warps); below that, and for small remainders, rounds of 4 rotations per SM
+    then SM pairs (148, 1185), 2-3 per SM (149-447, 1333, 2668) or a
+    4-rotation launch ending in a CTA of 1, 2 and 3 active rotations
+    (445-447; 3 is the phase-skewed case with a single trailing group, which
+    also refills the key ring)."""
     sk, _, bsk = desk_keys
     rng = np.random.default_rng(count)
     A, b = lwe.encrypt_batch(rng.integers(-511, 513, count), sk, desk, rng)
@@ -179,13 +182,15 @@ def test_n1024_three_level_gadget_paths():
             assert np.array_equal(oA[sl], wA) and np.array_equal(ob[sl], wb), count
 
 
-@pytest.mark.parametrize("count", [5, 400, 599])
+@pytest.mark.parametrize("count", [5, 400, 599, 1300])
 def test_desk_blind_rotate_raw_mode(desk, desk_keys, count):
-    """blind_rotate_batch at DESK through the latency kernel (5), the paired
-    kernel at 3 rotations per CTA (400) and the phase-skewed 4-rotation kernel
-    plus a latency-kernel tail (599), raw accumulators in and out, vs the
-    oracle.  Every third rotation starts with an identity step (rotation 0),
-    the skew's signalling path when it falls on a leading accumulator."""
+    """blind_rotate_batch at DESK through the CTA-pair kernel (5), the paired
+    kernel at 3 rotations per CTA (400), the phase-skewed 4-rotation kernel
+    plus a CTA-pair tail (599) and a warp-per-rotation wave plus a CTA-pair
+    tail (1300), raw accumulators in and out, vs the oracle.  Every third
+    rotation starts with an identity step (rotation 0): the skew's signalling
+    path when it falls on a leading accumulator, and a warp that skips a step
+    but still takes part in the key ring."""
     sk, _, bsk = desk_keys
     rng = np.random.default_rng(40 + count)
     acc = rng.integers(0, desk.q, (count, 2, desk.N))
