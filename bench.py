@@ -384,12 +384,13 @@ def run_b200(args, world, rank, local):
     br_launch_ms = br_ms / max(br_calls, 1)
     pbs_per_launch = BATCH * NEURONS * 2
     achieved = FLOPS_PER_PBS_DESK * pbs_per_launch / (br_launch_ms * 1e-3) / 1e12
-    traffic, pipe_active = None, None
+    traffic, pipe_active, traffic_pbs = None, None, None
     tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
         traffic = tj.get("bytes_per_launch")
         pipe_active = tj.get("fp64_pipe_active")
+        traffic_pbs = tj.get("pbs_per_launch")
 
     configs = None
     if world == 1 and not args.no_configs:
@@ -409,6 +410,9 @@ def run_b200(args, world, rank, local):
         "gpu_launches": kc.launches,
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "traffic_note": f"DRAM bytes of one pbs_br16_kernel launch ({traffic_pbs} PBS) from the committed "
+                                     "ncu capture (profiles/roofline_traffic.json); the key is read from DRAM about once "
+                                     "per launch (L2-resident), the rest is ciphertext rows",
                      "fp64_pipe_active": pipe_active,
                      "kernel": "blind rotation per fused LIF call (4096 PBS): pbs_br16_kernel, 3 waves of 8 "
                                "rotations per SM (3552) + pbs_blind_rotate_kernel<512,4,..> for the 544-rotation "

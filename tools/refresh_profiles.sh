@@ -13,7 +13,7 @@ CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
 if $CMD > $O/${TAG}_plain.json 2>&1; then
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
       --log-file $O/${TAG}_launches.csv $CMD > $O/${TAG}_ncu_launch.log 2>&1; echo "launch list rc=$?"
-  ncu --set full --clock-control none --import-source on -k regex:pbs_blind -s 6 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:pbs_br16 -s 3 -c 1 \
       -o $O/${TAG}_bench_br $CMD > $O/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
   tail -2 $O/${TAG}_ncu_full.log
 fi
