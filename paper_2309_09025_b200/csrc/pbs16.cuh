@@ -29,8 +29,11 @@
 namespace fdsnn {
 
 constexpr int BR16_MAXW = 8;   // warps (rotations) per CTA
-constexpr int BR16_S = 5;      // key ring stages
+constexpr int BR16_S = 4;      // key ring stages (3: 18% slower, 5: 0.7% slower)
 constexpr uint32_t BR16_CHUNK = 2u * 512u * sizeof(double2);
+// header: full[S], empty[S] mbarriers, release counters[S], TMEM address slot
+constexpr size_t BR16_HDR = 128;
+static_assert(20 * BR16_S + 8 <= BR16_HDR, "ring header");
 // TMEM columns per lane quadrant: the lane table (7 x 32, shared by warps w
 // and w + 4), then per warp (w / 4 = 0, 1) the partial spectra of both output
 // polynomials after the first digit pair (2 x 64).
@@ -41,7 +44,7 @@ __host__ __device__ constexpr size_t br16_warp_bytes(int n) {
     return 2 * 1024 * sizeof(int32_t) + r16::XBUF * sizeof(double2) + (((size_t)n * 2 + 15) & ~(size_t)15);
 }
 __host__ __device__ constexpr size_t br16_smem_bytes(int G, int n) {
-    return 128 + (size_t)BR16_S * BR16_CHUNK + (size_t)G * br16_warp_bytes(n);
+    return BR16_HDR + (size_t)BR16_S * BR16_CHUNK + (size_t)G * br16_warp_bytes(n);
 }
 
 template <bool MODE_RAW, bool TRACK_MARGIN>
@@ -55,12 +58,12 @@ __global__ void __launch_bounds__(BR16_MAXW * 32, 1) pbs_br16_kernel(const PbsAr
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);          // [S] stage landed
     uint64_t* empty = full + S;                                       // [S] stage released by every warp
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw + 96);       // [S] releases so far
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(smem_raw + 120);
-    double2* ring = reinterpret_cast<double2*>(smem_raw + 128);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw + 16 * S);   // [S] releases so far
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(smem_raw + BR16_HDR - 8);
+    double2* ring = reinterpret_cast<double2*>(smem_raw + BR16_HDR);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = blockDim.x >> 5;
-    unsigned char* mine = smem_raw + 128 + S * CHUNK + warp * br16_warp_bytes(n);
+    unsigned char* mine = smem_raw + BR16_HDR + S * CHUNK + warp * br16_warp_bytes(n);
     int32_t* acc = reinterpret_cast<int32_t*>(mine);                  // [2][N]
     double2* xbuf = reinterpret_cast<double2*>(mine + 2 * N * sizeof(int32_t));
     uint16_t* a2N = reinterpret_cast<uint16_t*>(mine + 2 * N * sizeof(int32_t) + r16::XBUF * sizeof(double2));
