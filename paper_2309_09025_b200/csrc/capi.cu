@@ -620,7 +620,10 @@ int fdsnn_ctx_create(const fdsnn_params* prm, int32_t device, fdsnn_ctx** out) {
         std::vector<double2> tab(M);
         for (int k = 0; k < M; ++k) {
             long double tw = PI * k / p.N;
-            tab[k] = make_double2((double)cosl(tw), (double)sinl(tw));
+            // M = 1024: points k = 3 mod 4 (odd-parity lanes t' odd) carry the
+            // (-1)^{t'} of the balanced radix-2 join (fft.cuh r2_join)
+            const long double sg = (M == 1024 && k % 4 == 3) ? -1.0L : 1.0L;
+            tab[k] = make_double2((double)(sg * cosl(tw)), (double)(sg * sinl(tw)));
         }
         {
             // M = 1024 runs as two 512-point transforms (fft.cuh parity split):

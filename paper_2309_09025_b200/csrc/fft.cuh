@@ -449,12 +449,14 @@ FDSNN_DEV void fft_stockham2p(double2 (&v0)[8], double2 (&v1)[8], int t, const T
 // the even and odd lanes, each parity in its own half of the exchange
 // buffers) are joined by one radix-2 step between lanes 2t' and 2t'+1 through
 // warp shuffles:  X[k] = E[k] + w^k O[k],  X[k + 512] = E[k] - w^k O[k]
-// (w = e^{+2 pi i/1024}; the inverse runs the mirrored steps with conj(w)).
+// (w = e^{+2 pi i/1024}; the inverse runs the mirrored steps with conj(w)),
+// balanced so each lane ships 4 values (r2_join below).
 // Against the 4-pass Stockham schedule (8,4,4,8) this trades one
-// shared-memory exchange and its barrier for 32 shuffles per thread.
-// Output layout: even lanes hold X[t' + 64 r], odd lanes X[t' + 64 r + 512];
-// the Fourier key is produced by the same transform, so the MAC (thread t
-// reads key index t + 128 r) pairs matching frequencies.
+// shared-memory exchange and its barrier for 16 shuffles per thread.
+// Output layout: lane (t', p), register r < 4 / r + 4 holds (a unit multiple
+// of) X[k] / X[k + 512], k = t' + 64 (r + 4p); the Fourier key is produced by
+// the same transform (and scaled back to the true basis), so the MAC (thread
+// t reads key index t + 128 r) pairs matching frequencies.
 constexpr int FFT1024_HALF = 580;  // odd-parity region offset: 576 (padded 512 points) + 4 slots
 
 template <>
@@ -486,39 +488,46 @@ FDSNN_DEV double2 shfl_xor1(double2 a) {
     return make_double2(__shfl_xor_sync(0xffffffffu, a.x, 1), __shfl_xor_sync(0xffffffffu, a.y, 1));
 }
 
-// The radix-2 factor provider returns w^k on odd lanes and 1 on even lanes,
-// so both lanes run the same instructions (no selects): the odd lane
-// pre-multiplies its O by w^k, the lanes swap, and X = partner + s * own with
-// s = +1 (even) / -1 (odd).
-// forward: lanes hold E (even) / O (odd) -> X[k] (even) / X[k+512] (odd)
+// Balanced, select-free radix-2 join (the fft16.cuh construction): the even
+// lane finishes k = t' + 64 r for r < 4, the odd lane r >= 4, each sending 4
+// of its 8 values.  The odd lane's 512-point inputs carry (-1)^{t'} (folded
+// into the twist table: points j = 3 mod 4), which rotates its outputs by
+// 4 registers, so every lane keeps registers 0-3 and ships 4-7; then
+// out0 = P + z Q, out1 = P - z Q with z = w^k (even lane, k = t' + 64 r) or
+// w^{-k} (odd lane, k = t' + 64 (r + 4)).  The odd lane thus holds
+// w^{-k} X[k] and -w^{-k} X[k + 512]: the inverse's first step consumes
+// exactly that scaling, and the Fourier key (bsk_forward_kernel) is stored in
+// the true basis.  The provider returns the 4 factors z.
+// forward: E (even lanes) / O (odd lanes) -> X, registers r < 4: k, r + 4: k + 512
 template <class TW>
-FDSNN_DEV void r2_join(double2 (&v)[8], int p, const TW& tw) {
+FDSNN_DEV void r2_join(double2 (&v)[8], int /*p*/, const TW& tw) {
     uint32_t raw[32];
     tw.issue_r2(raw);
-    double2 w[8];
-    tw.finish_r2(raw, w);
-    const double s = p ? -1.0 : 1.0;
+    double2 z[8];
+    tw.finish_r2(raw, z);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const double2 own = cmul(v[r], w[r]);
-        const double2 o = shfl_xor1(own);
-        v[r] = make_double2(fma(s, own.x, o.x), fma(s, own.y, o.y));
+    for (int r = 0; r < 4; ++r) {
+        const double2 q = shfl_xor1(v[r + 4]);
+        const double2 y = cfma<false>(v[r], z[r], q);
+        v[r + 4] = ctwo_minus(v[r], y);
+        v[r] = y;
     }
 }
-// inverse: lanes hold X[k] (even) / X[k+512] (odd) -> E' (even) / O' (odd)
+// inverse: the join's output layout and scaling -> E' (even lanes) / O'
+// rotated by 4 registers (odd lanes; its sign is cancelled by the twist)
 template <class TW>
-FDSNN_DEV void r2_split(double2 (&v)[8], int p, const TW& tw) {
+FDSNN_DEV void r2_split(double2 (&v)[8], int /*p*/, const TW& tw) {
     uint32_t raw[32];
     tw.issue_r2(raw);
-    double2 o[8];
+    double2 z[8];
+    tw.finish_r2(raw, z);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) o[r] = shfl_xor1(v[r]);
-    double2 w[8];
-    tw.finish_r2(raw, w);
-    const double s = p ? -1.0 : 1.0;
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-        v[r] = cmulc(make_double2(fma(s, v[r].x, o[r].x), fma(s, v[r].y, o[r].y)), w[r]);
+    for (int r = 0; r < 4; ++r) {
+        const double2 mine = cadd(v[r], v[r + 4]);
+        const double2 send = cmulc(csub(v[r], v[r + 4]), z[r]);
+        v[r] = mine;
+        v[r + 4] = shfl_xor1(send);
+    }
 }
 
 template <int M, bool INV, class TW, class HOOK = NoHook, bool FT0 = false>

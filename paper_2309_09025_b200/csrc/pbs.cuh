@@ -122,8 +122,16 @@ FDSNN_DEV void load_tw_regs(TwiddlesInRegs<M>& tw, int t, const double2* __restr
         load_twiddles<512>(tw.half.tw, t >> 1, tables + 1024);
         const double2* r2 = tables + 1024 + twiddle_table_size<512>();
 #pragma unroll
-        for (int r = 0; r < 8; ++r)  // odd lanes: w^{t' + 64 r}; even lanes: 1 (fft.cuh r2_join)
-            tw.r2[r] = (t & 1) ? __ldg(r2 + (t >> 1) + 64 * r) : make_double2(1.0, 0.0);
+        for (int r = 0; r < 8; ++r) {  // join factors (fft.cuh r2_join): w^{t'+64r} (even), w^{-(t'+64(r+4))} (odd)
+            if (r >= 4) {
+                tw.r2[r] = make_double2(0.0, 0.0);
+            } else if (t & 1) {
+                const double2 w = __ldg(r2 + (t >> 1) + 64 * (r + 4));
+                tw.r2[r] = make_double2(w.x, -w.y);
+            } else {
+                tw.r2[r] = __ldg(r2 + (t >> 1) + 64 * r);
+            }
+        }
     } else {
         load_twiddles<M>(tw.tw, t, tables + M);
     }
@@ -918,6 +926,18 @@ bsk_forward_kernel(const int64_t* __restrict__ rows, int64_t npoly, int log2q,
     }
     int ex = 0;
     fft_group<M, false>(vv, t, tw, buf0, buf1, ex, gs);
+    if constexpr (M == 1024) {
+        // odd lanes hold s X, s = z_r (register r) / -z_r (r + 4): back to the
+        // true basis (fft.cuh r2_join)
+        if (t & 1) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                vv[r] = cmulc(vv[r], tw.r2[r]);
+                const double2 x = cmulc(vv[r + 4], tw.r2[r]);
+                vv[r + 4] = make_double2(-x.x, -x.y);
+            }
+        }
+    }
     const double inv_m = 1.0 / M;
 #pragma unroll
     for (int r = 0; r < 8; ++r)
