@@ -23,6 +23,7 @@
 #include "pbs.cuh"
 #include "pbs_cluster.cuh"
 #include "pbs16.cuh"
+#include "lin_umma.cuh"
 #include "plain.cuh"
 #include "lwe_dev.cuh"
 #include "ring_ops.cuh"
@@ -76,6 +77,9 @@ struct Operator {
     bool dense = true;
     int out_cells = 0, in_cells = 0;
     int32_t* w = nullptr;        // dense (out x in)
+    // dense with s8 weights: tensor-core path (lin_umma.cuh), A tiles
+    uint8_t* at = nullptr;
+    int lin_ksteps = 0, lin_rblocks = 0;
     int32_t* row_ptr = nullptr;  // csr
     int32_t* col_idx = nullptr;
     int32_t* val = nullptr;
@@ -109,7 +113,7 @@ struct fdsnn_ctx {
     // digit tiles), so launches on different streams never share buffers.
     // `stage`: device staging of the client-side encrypt/decrypt entry points;
     // `pin`: page-locked slots of the int64 host boundary (hostio.h).
-    struct StreamScratch { Buf ext, ks_dig, stage; PinnedSlots pin; };
+    struct StreamScratch { Buf ext, ks_dig, stage, lin_b; PinnedSlots pin; };
     std::map<cudaStream_t, StreamScratch> scratch;
     int64_t wide_max = 148;  // largest batch routed to the latency kernel (FDSNN_WIDE_MAX)
     // CTA-pair kernel (pbs_cluster.cuh): one rotation per SM pair up to
@@ -675,7 +679,7 @@ int fdsnn_ctx_destroy(fdsnn_ctx* ctx) {
         if (ctx->stream) cudaStreamSynchronize(ctx->stream);
         for (auto& t : ctx->timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
         for (auto* l : ctx->luts) cudaFree(l);
-        for (auto& o : ctx->ops) { cudaFree(o.w); cudaFree(o.row_ptr); cudaFree(o.col_idx); cudaFree(o.val); }
+        for (auto& o : ctx->ops) { cudaFree(o.w); cudaFree(o.at); cudaFree(o.row_ptr); cudaFree(o.col_idx); cudaFree(o.val); }
         cudaFree(ctx->tables);
         cudaFree(ctx->tab16);
         cudaFree(ctx->bsk16);
@@ -686,6 +690,7 @@ int fdsnn_ctx_destroy(fdsnn_ctx* ctx) {
         for (auto& kv : ctx->scratch) {
             kv.second.ext.release();
             kv.second.ks_dig.release();
+            kv.second.lin_b.release();
             kv.second.stage.release();
             kv.second.pin.release();
         }
@@ -1090,9 +1095,28 @@ int fdsnn_operator_load(fdsnn_ctx* ctx, const int64_t* Mh, int64_t out_cells, in
         op.dense = nnz * 4 > total;
         if (op.dense) {
             std::vector<int32_t> w((size_t)total);
-            for (int64_t i = 0; i < total; ++i) w[i] = (int32_t)Mh[i];
+            bool s8 = true;
+            for (int64_t i = 0; i < total; ++i) {
+                w[i] = (int32_t)Mh[i];
+                s8 = s8 && w[i] >= -128 && w[i] <= 127;
+            }
             CU(cudaMalloc(&op.w, w.size() * 4));
             CU(cudaMemcpy(op.w, w.data(), w.size() * 4, cudaMemcpyHostToDevice));
+            // tensor-core path: s8 weights, 4 byte limbs cover q, exact s32 sums
+            const char* e = getenv("FDSNN_LIN_CUDACORE");
+            const int kq = KSU_KSTEP * KSU_KPS;
+            const int64_t kpad = (in_cells + kq - 1) / kq * kq;
+            if (s8 && !(e && atoi(e) == 1) && ctx->dp.log2q <= 8 * LIN_LIMBS &&
+                (double)kpad * 128.0 * 255.0 < 2147483647.0) {
+                op.lin_ksteps = (int)(kpad / KSU_KSTEP);
+                op.lin_rblocks = (int)((out_cells + KSU_M - 1) / KSU_M);
+                const int64_t segs = (int64_t)op.lin_rblocks * op.lin_ksteps * KSU_M * 2;
+                CU(cudaMalloc(&op.at, (size_t)op.lin_rblocks * op.lin_ksteps * KSU_A_STEP));
+                lin_prepare_a_kernel<<<grid1d(segs), 256>>>(op.w, op.out_cells, op.in_cells, op.lin_ksteps,
+                                                            op.lin_rblocks, op.at);
+                CU(cudaGetLastError());
+                CU(cudaDeviceSynchronize());
+            }
         } else {
             std::vector<int32_t> rp(out_cells + 1), ci, va;
             ci.reserve(nnz);
@@ -1133,6 +1157,31 @@ int operator_apply_impl(fdsnn_ctx* ctx, int32_t op_id, const uint32_t* d_in, int
     const Operator& op = ctx->ops[op_id];
     const DevParams& d = ctx->dp;
     TimerScope ts(ctx, 2, s);
+    if (op.at) {  // tensor-core weight sum (lin_umma.cuh): limb tiles of X, then the GEMM
+        const int64_t ncols = batch * d.stride, ctiles = (ncols + KSU_COLS - 1) / KSU_COLS;
+        Buf& bbuf = ctx->scratch[s].lin_b;
+        int rc = bbuf.ensure((size_t)ctiles * op.lin_ksteps * LINU_B_STEP);
+        if (rc) return rc;
+        uint8_t* bt = reinterpret_cast<uint8_t*>(bbuf.p);
+        lin_prepare_b_kernel<<<grid1d(ctiles * KSU_COLS * op.lin_ksteps * 2), 256, 0, s>>>(
+            d_in, op.in_cells, d.stride, ncols, op.lin_ksteps, ctiles, bt);
+        CU(cudaGetLastError());
+        LinUmmaArgs u{};
+        u.at = op.at;
+        u.bt = bt;
+        u.ksteps = op.lin_ksteps;
+        u.out_cells = op.out_cells;
+        u.stride = d.stride;
+        u.ncols = ncols;
+        u.qmask = d.qmask;
+        u.Y = d_out;
+        const size_t smem = ksu_smem_bytes(LIN_LIMBS);
+        CU(cudaFuncSetAttribute(lin_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        lin_umma_kernel<<<dim3((unsigned)ctiles, (unsigned)op.lin_rblocks), 128, smem, s>>>(u);
+        CU(cudaGetLastError());
+        ts.kernels = 2;
+        return FDSNN_OK;
+    }
     if (op.dense) {
         // full 128-column tiles on the tiled kernel; a tail of at most one
         // 16-byte column group (DESK: b + 3 pad words after 512 mask columns)

@@ -176,3 +176,31 @@ def test_layer_forward(desk, desk_keys, dense):
     out = network.layer_forward(network.CiphertextTensor((M.shape[1],), A, b, desk.q), layer, desk)
     wA, wb = O.layer_forward(M, A, b, desk.q)
     assert np.array_equal(out.A, wA) and np.array_equal(out.b, wb)
+
+
+@pytest.mark.parametrize("wmax,cudacore", [(127, False), (127, True), (200, False)])
+def test_layer_forward_tensor_core_and_fallback(desk, desk_keys, wmax, cudacore, monkeypatch):
+    """Dense weight sums: s8 weights run on the tcgen05 kind::i8 GEMM
+    (lin_umma.cuh: 4 byte limbs of every ciphertext word, exact s32 sums);
+    FDSNN_LIN_CUDACORE=1, or any weight outside [-128, 127], selects the
+    CUDA-core int32 GEMM.  Shapes exercise every padding: 130 outputs (a
+    partial second row block), 300 inputs (K padded to 384), 3 samples (1548
+    columns: a partial last column tile), extreme weights +-127 / -128."""
+    from paper_2309_09025_b200.device import DeviceContext
+    if cudacore:
+        monkeypatch.setenv("FDSNN_LIN_CUDACORE", "1")
+    sk, _, _ = desk_keys
+    rng = np.random.default_rng(60 + wmax)
+    M = rng.integers(-wmax, wmax + 1, (130, 300))
+    M[0, :4] = [127, -128, 127, -128] if wmax == 127 else [wmax, -wmax, 1, -1]
+    xs = []
+    for s in range(3):
+        ms, A, b = _enc(desk, sk, 300, 70 + s, 0, 1)
+        xs.append(network.CiphertextTensor((300,), A, b, desk.q))
+    dev = DeviceContext(desk)  # fresh context: the operator is loaded under this test's environment
+    op = dev.operator(M)
+    rows = dev.rows_from_host_parts([(x.A, x.b) for x in xs])
+    A, b = dev.rows_to_host(dev.apply(op, rows, 3, 130))
+    for s in range(3):
+        wA, wb = O.layer_forward(M, xs[s].A, xs[s].b, desk.q)
+        assert np.array_equal(A[s * 130:(s + 1) * 130], wA) and np.array_equal(b[s * 130:(s + 1) * 130], wb), s
