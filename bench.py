@@ -444,9 +444,10 @@ def run_b200(args, world, rank, local):
 def run_e2e_int64(args, api, prm, bsk, lif, Wm, A, b, sk, g1):
     """The headline step through the reference's own call signatures on host
     int64 arrays: per timestep, the 16 samples' weight sums
-    (network.layer_forward_batch: each result equals layer_forward, network.py:409-421)
-    then one spiking_forward over the 2048 stacked cells (network.py:430-436)
-    carrying the states; results come back as host CiphertextTensors."""
+    (network.layer_forward_batch: each result equals layer_forward, network.py:409-421,
+    returned stacked as one (16, 128) tensor) then one spiking_forward over the
+    2048 cells (network.py:430-436) carrying the states; results come back as
+    host CiphertextTensors."""
     import torch
     N = api.network
     layer = N.WeightLayer("linear", Wm, None, 1.0, (NEURONS,))
@@ -460,9 +461,7 @@ def run_e2e_int64(args, api, prm, bsk, lif, Wm, A, b, sk, g1):
         states = N.zero_states(BATCH * NEURONS, prm)
         spikes = []
         for t in range(T_STEPS):
-            cur = N.layer_forward_batch(xs[t], layer, prm)
-            stacked = N.CiphertextTensor((BATCH * NEURONS,), np.concatenate([c.A for c in cur]),
-                                         np.concatenate([c.b for c in cur]), prm.q)
+            stacked = N.layer_forward_batch(xs[t], layer, prm, stack=True)  # (16, 128) cells
             sp, states = N.spiking_forward(stacked, states, lif, bsk)
             spikes.append(sp)
         return spikes

@@ -71,15 +71,17 @@ def test_parameter_errors(desk, desk_keys):
         network.layer_forward(x, layer, desk)
 
 
-@pytest.mark.parametrize("which,bound", [("desk", 0.01), ("c4prm", 0.01)])
-def test_transform_exactness_margin(which, bound, request):
+@pytest.mark.parametrize("which,count,bound", [("desk", 64, 0.01), ("desk", 1184, 0.01), ("c4prm", 64, 0.01)])
+def test_transform_exactness_margin(which, count, bound, request):
     """max |x - round(x)| over every rounded product of every CMux step stays far
     below 0.5 (the condition under which FP64 transforms are exact and the
-    device's round-to-nearest equals the reference's round-half-away)."""
+    device's round-to-nearest equals the reference's round-half-away).  DESK
+    64: the CTA-pair kernel; DESK 1184: one wave of the warp-per-rotation
+    kernel (fft16.cuh); C4: the 4-per-SM kernel's parity-split transform."""
     prm = request.getfixturevalue(which)
     sk, _, bsk = request.getfixturevalue("desk_keys" if which == "desk" else "c4_keys")
     rng = np.random.default_rng(9)
-    A, b = lwe.encrypt_batch(rng.integers(-prm.p // 2 + 1, prm.p // 2 + 1, 64), sk, prm, rng)
+    A, b = lwe.encrypt_batch(rng.integers(-prm.p // 2 + 1, prm.p // 2 + 1, count), sk, prm, rng)
     dev = bsk.device
     dev.margin(True)
     try:

@@ -36,6 +36,9 @@ def test_layer_forward_identity_pool_and_conv(toy, toy_keys, toy64, toy64_keys):
     outs = network.layer_forward_batch([x for _, x in xs], layer, toy64)
     for (msgs, _), out in zip(xs, outs):
         assert np.array_equal(lwe.decrypt_batch(out.A, out.b, sk64, toy64), m @ msgs)
+    st = network.layer_forward_batch([x for _, x in xs], layer, toy64, stack=True)
+    assert st.shape == (10, *layer.out_shape)
+    assert np.array_equal(st.A, np.concatenate([o.A for o in outs])) and np.array_equal(st.b, np.concatenate([o.b for o in outs]))
 
 
 @pytest.fixture(scope="module")
