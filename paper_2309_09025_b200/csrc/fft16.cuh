@@ -49,17 +49,36 @@ namespace r16 {
 constexpr int M = 512;
 constexpr int XSTRIDE = 34;            // exchange row stride (complex) per k2
 constexpr int XBUF = 16 * XSTRIDE;     // complex per warp exchange buffer
-// Per-lane constant table: 7 blocks of 8 complex (32 words = 32 TMEM
-// columns each), lane-major [lane][TAB] in global memory.
-constexpr int BLK_TW_E = 0;  // sigma_l e^{i pi p/N}, p = l + 32 j2, even j2 (sigma = -1 for l = 3 mod 4)
-constexpr int BLK_TW_O = 1;  //   odd j2
-constexpr int BLK_FB_E = 2;  // w512^{(a + 2b) k2'} (lane = 2 k2' + a), even b
-constexpr int BLK_FB_O = 3;  //   odd b
-constexpr int BLK_IA_E = 4;  // w512^{l k2} (inverse pass A, used conjugated), even k2
-constexpr int BLK_IA_O = 5;  //   odd k2
-constexpr int BLK_ZJ = 6;    // a = 0: w32^r, a = 1: w32^{-(r+8)}, r < 8
-constexpr int NBLK = 7;
+// Twist factorisation.  The twist of point p = l + 32 j2 splits into a lane
+// factor and a register factor: sigma_l e^{i pi p/N} = c_l g_{j2} with
+// c_l = sigma_l e^{i pi l/N} (sigma = -1 for l = 3 mod 4, see the join) and
+// g_{j2} = e^{i pi j2/32} (N = 1024).  Pass A (a DFT over j2 inside lane l)
+// applies only g -- compile-time constants, no table -- and commutes with the
+// lane constant c_l, which is folded into pass B's twiddles:
+//   FB[L][b] = w512^{(a + 2b) k2'} c_{a + 2b}      (lane L = 2 k2' + a).
+// The inverse mirrors the forward: its first DFT16 (over b in lane L) is
+// followed by the conjugates of the same FB factors (the inter-pass twiddles
+// of the inverse and the untwist's lane factor conj(c_l) at once), the return
+// exchange, a twiddle-free DFT16 over k2 and the register untwist conj(g_j2).
+// Per-lane constant table: 3 blocks of 8 complex (32 words = 32 TMEM columns
+// each), lane-major [lane][TAB] in global memory.
+constexpr int BLK_FB_E = 0;  // FB[L][b], even b
+constexpr int BLK_FB_O = 1;  //   odd b
+constexpr int BLK_ZJ = 2;    // a = 0: w32^r, a = 1: w32^{-(r+8)}, r < 8
+constexpr int NBLK = 3;
 constexpr int TAB = 8 * NBLK;
+
+// g_j = e^{i pi j/32}, j < 16
+FDSNN_DEV constexpr double g_cos(int j) {
+    constexpr double c[16] = {1.0, 0.995184726672196886245, 0.980785280403230449126, 0.956940335732208864936,
+                              0.923879532511286756128, 0.881921264348355029713, 0.831469612302545237079,
+                              0.773010453362736960811, 0.707106781186547524401, 0.634393284163645498215,
+                              0.555570233019602224743, 0.471396736825997648556, 0.382683432365089771728,
+                              0.290284677254462367636, 0.195090322016128267848, 0.098017140329560601994};
+    return c[j];
+}
+FDSNN_DEV constexpr double g_sin(int j) { return j == 0 ? 0.0 : g_cos(16 - j); }
+FDSNN_DEV double2 g_twist(int j) { return make_double2(g_cos(j), j == 0 ? 0.0 : g_cos(16 - j)); }
 
 // Table providers: issue(blk, raw) starts fetching block blk (8 complex),
 // finish(raw, w) completes it.
@@ -113,10 +132,13 @@ FDSNN_DEV void radix2_16(double2 (&v)[16], const double2 (&e)[8], const double2 
     }
 }
 
+constexpr int TWIST_G = -2;  // dft16 BLK value: input twiddles g_j (constants)
+
 // 16-point DFT, natural order in/out, kernel e^{+2 pi i/16} (INV: e^{-}).
 // BLK >= 0: the input twiddles of table blocks BLK (even points) and BLK + 1
 // (odd points) are fused into the first butterflies (conjugated when INV),
-// as dft8_tw does for radix 8.
+// as dft8_tw does for radix 8; BLK == TWIST_G: the constants g_j instead
+// (g_0 = 1 is skipped).
 template <bool INV, int BLK, class TP>
 FDSNN_DEV void dft16(double2 (&v)[16], const TP& tp) {
     double2 e[8], o[8];
@@ -139,6 +161,15 @@ FDSNN_DEV void dft16(double2 (&v)[16], const TP& tp) {
         dft8_tw<INV, true>(e, w);
         tp.finish(ro, w);
         dft8_tw<INV, true>(o, w);
+    } else if constexpr (BLK == TWIST_G) {
+        double2 we[7], wo[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            if (r > 0) we[r - 1] = g_twist(2 * r);
+            wo[r] = g_twist(2 * r + 1);
+        }
+        dft8_tw<INV, false>(e, we);
+        dft8_tw<INV, true>(o, wo);
     } else {
         dft8<INV>(e);
         dft8<INV>(o);
@@ -156,7 +187,7 @@ FDSNN_DEV double2 shfl_xor1c(double2 a) {
 // xbuf: the warp's exchange buffer.
 template <class TP>
 FDSNN_DEV void forward(double2 (&v)[16], int lane, const TP& tp, double2* __restrict__ xbuf) {
-    dft16<false, BLK_TW_E>(v, tp);
+    dft16<false, TWIST_G>(v, tp);
     __syncwarp();  // the previous transform's readers of xbuf are done
 #pragma unroll
     for (int k = 0; k < 16; ++k) xbuf[k * XSTRIDE + lane] = v[k];
@@ -182,8 +213,8 @@ FDSNN_DEV void forward(double2 (&v)[16], int lane, const TP& tp, double2* __rest
 
 // Inverse transform (unnormalised, kernel e^{-2 pi i jk/M}) of one polynomial.
 //   in:  v in the forward's output layout and scaling
-//   out: v[j2] = M * point l + 32 j2 times sigma_l (cancelled by the signed
-//        conjugate twist applied by the caller)
+//   out: v[j2] = M * point l + 32 j2 times g_{j2} (the caller untwists with
+//        conj(g_{j2}); the lane factor conj(c_l) is already applied)
 template <class TP>
 FDSNN_DEV void inverse(double2 (&v)[16], int lane, const TP& tp, double2* __restrict__ xbuf) {
     {
@@ -200,6 +231,18 @@ FDSNN_DEV void inverse(double2 (&v)[16], int lane, const TP& tp, double2* __rest
         }
     }
     dft16<true, -1>(v, tp);
+    {  // output twiddles conj(FB[L][b]): even b, then odd b
+        uint32_t re[32], ro[32];
+        double2 w[8];
+        tp.issue(BLK_FB_E, re);
+        tp.issue(BLK_FB_O, ro);
+        tp.finish(re, w);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[2 * r] = cmulc(v[2 * r], w[r]);
+        tp.finish(ro, w);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[2 * r + 1] = cmulc(v[2 * r + 1], w[r]);
+    }
     __syncwarp();
     const int row = (lane >> 1) * XSTRIDE + (lane & 1);
 #pragma unroll
@@ -207,16 +250,7 @@ FDSNN_DEV void inverse(double2 (&v)[16], int lane, const TP& tp, double2* __rest
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = xbuf[k * XSTRIDE + lane];
-    dft16<true, BLK_IA_E>(v, tp);
-}
-
-// The signed twist of point j2 of this lane (for the caller's untwist:
-// multiply by its conjugate).
-template <class TP>
-FDSNN_DEV void twist_block(const TP& tp, int half, double2 (&w)[8]) {
-    uint32_t raw[32];
-    tp.issue(BLK_TW_E + half, raw);
-    tp.finish(raw, w);
+    dft16<true, -1>(v, tp);
 }
 
 // Host-side construction of the per-lane table (long double, ring.py:115-118
@@ -225,21 +259,19 @@ template <class C, class MK>
 inline void build_table(int N, C* out, MK make) {
     const long double PI = 3.141592653589793238462643383279502884L;
     auto at = [&](int l, int blk, int i) -> C& { return out[l * TAB + 8 * blk + i]; };
-    for (int l = 0; l < 32; ++l) {
-        const long double sg = (l % 4 == 3) ? -1.0L : 1.0L;
-        const int k2p = l >> 1, a = l & 1;
-        for (int j = 0; j < 16; ++j) {
-            const long double ang = PI * (l + 32 * j) / N;
-            at(l, BLK_TW_E + (j & 1), j >> 1) = make(sg * cosl(ang), sg * sinl(ang));
-            const long double af = 2.0L * PI * (long double)(((a + 2 * j) * k2p) % M) / M;
-            at(l, BLK_FB_E + (j & 1), j >> 1) = make(cosl(af), sinl(af));
-            const long double ai = 2.0L * PI * (long double)((l * j) % M) / M;
-            at(l, BLK_IA_E + (j & 1), j >> 1) = make(cosl(ai), sinl(ai));
+    for (int L = 0; L < 32; ++L) {
+        const int k2p = L >> 1, a = L & 1;
+        for (int b = 0; b < 16; ++b) {
+            const int l = a + 2 * b;  // source lane of register b
+            const long double sg = (l % 4 == 3) ? -1.0L : 1.0L;
+            // w512^{l k2'} c_l, c_l = sigma_l e^{i pi l / N}
+            const long double ang = 2.0L * PI * (long double)((l * k2p) % M) / M + PI * l / N;
+            at(L, BLK_FB_E + (b & 1), b >> 1) = make(sg * cosl(ang), sg * sinl(ang));
         }
         for (int r = 0; r < 8; ++r) {
             const int e = a ? -(r + 8) : r;
             const long double ang = 2.0L * PI * e / 32.0L;
-            at(l, BLK_ZJ, r) = make(cosl(ang), sinl(ang));
+            at(L, BLK_ZJ, r) = make(cosl(ang), sinl(ang));
         }
     }
 }

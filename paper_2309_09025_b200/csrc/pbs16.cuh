@@ -34,11 +34,13 @@ constexpr uint32_t BR16_CHUNK = 2u * 512u * sizeof(double2);
 // header: full[S], empty[S] mbarriers, release counters[S], TMEM address slot
 constexpr size_t BR16_HDR = 128;
 static_assert(20 * BR16_S + 8 <= BR16_HDR, "ring header");
-// TMEM columns per lane quadrant: the lane table (7 x 32, shared by warps w
-// and w + 4), then per warp (w / 4 = 0, 1) the partial spectra of both output
-// polynomials after the first digit pair (2 x 64).
+// TMEM columns per lane quadrant: the lane table (3 x 32, shared by warps w
+// and w + 4), then per warp (w / 4 = 0, 1) 192 columns: the partial spectra of
+// output polynomials 0 and 1 (2 x 64) and the warp's own accumulator
+// coefficients (2 x 32).
 constexpr uint32_t BR16_TMEM_COLS = 512;
-constexpr uint32_t BR16_COL_P = 7 * 32;
+constexpr uint32_t BR16_COL_P = r16::NBLK * 32;
+static_assert(BR16_COL_P + 2 * 192 <= BR16_TMEM_COLS, "TMEM columns");
 
 __host__ __device__ constexpr size_t br16_warp_bytes(int n) {
     return 2 * 1024 * sizeof(int32_t) + r16::XBUF * sizeof(double2) + (((size_t)n * 2 + 15) & ~(size_t)15);
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(BR16_MAXW * 32, 1) pbs_br16_kernel(const PbsAr
     if (active) {
         const int64_t v = vb + warp;
         const r16::TabTmem tp{lb};
-        const uint32_t p_col = lb + BR16_COL_P + 128 * (uint32_t)(warp >> 2);  // [poly 0 | poly 1] x 64
+        const uint32_t p_col = lb + BR16_COL_P + 192 * (uint32_t)(warp >> 2);  // [poly 0 | poly 1] x 64 | own
 
         // ---------------- setup: modulus switch + accumulator init -------------
         if constexpr (!MODE_RAW) {
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(BR16_MAXW * 32, 1) pbs_br16_kernel(const PbsAr
         }
         __syncwarp();
         {  // own coefficients -> TMEM: word 2 j2 = coef lane + 32 j2, word 2 j2 + 1 = coef lane + 32 j2 + M
-            const uint32_t own_col = p_col + 64;
+            const uint32_t own_col = p_col + 128;
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc) {
                 uint32_t w[32];
@@ -184,8 +186,7 @@ __global__ void __launch_bounds__(BR16_MAXW * 32, 1) pbs_br16_kernel(const PbsAr
         double err_max = 0.0;
 
         int c = 0;  // chunk = 4 i + 2 cc + lvl
-        const uint32_t p1_col = p_col;        // output poly 1 spectrum (64 words)
-        const uint32_t own_col = p_col + 64;  // own accumulator coefficients (2 x 32 words)
+        const uint32_t own_col = p_col + 128;  // own accumulator coefficients (2 x 32 words)
 #pragma unroll 1
         for (int i = 0; i < n; ++i) {
             const int k = a2N[i];
@@ -197,7 +198,6 @@ __global__ void __launch_bounds__(BR16_MAXW * 32, 1) pbs_br16_kernel(const PbsAr
                 }
                 continue;
             }
-            double2 P0[16];
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc) {
                 uint32_t dpk[16];  // level-1 digits, (coef p | coef p + M << 16)
@@ -246,31 +246,30 @@ __global__ void __launch_bounds__(BR16_MAXW * 32, 1) pbs_br16_kernel(const PbsAr
                     const int s = c % S;
                     mbar_wait(&full[s], (uint32_t)((c / S) & 1));
                     const double2* K = ring + (size_t)s * 1024 + lane;
-                    uint32_t w[32];
-                    if (f > 0) tmem_ld32_async(p1_col, w);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        if (f == 0) P0[j] = cmul(vv[j], K[32 * j]);
-                        else cmac(P0[j], vv[j], K[32 * j]);
-                    }
+                    // MAC into both output spectra (TMEM, 64 columns each)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
+                        const uint32_t col = p_col + 64 * h;
+                        uint32_t w0[32], w1[32];
                         if (f > 0) {
-                            if (h == 1) tmem_ld32_async(p1_col + 32, w);
-                            tmem_wait32(w);
+                            tmem_ld32_async(col, w0);
+                            tmem_ld32_async(col + 32, w1);
+                            tmem_wait64(w0, w1);
                         }
 #pragma unroll
-                        for (int jj = 0; jj < 8; ++jj) {
-                            const int j = 8 * h + jj;
+                        for (int j = 0; j < 16; ++j) {
+                            const double2 kk = K[512 * h + 32 * j];
                             double2 q;
-                            if (f == 0) q = cmul(vv[j], K[512 + 32 * j]);
+                            if (f == 0) q = cmul(vv[j], kk);
                             else {
-                                q = words_c(w, jj);
-                                cmac(q, vv[j], K[512 + 32 * j]);
+                                q = j < 8 ? words_c(w0, j) : words_c(w1, j - 8);
+                                cmac(q, vv[j], kk);
                             }
-                            put_words_c(w, jj, q);
+                            if (j < 8) put_words_c(w0, j, q);
+                            else put_words_c(w1, j - 8, q);
                         }
-                        tmem_st32(p1_col + 32 * h, w);
+                        tmem_st32(col, w0);
+                        tmem_st32(col + 32, w1);
                     }
                     release(c);
                     tmem_wait_st();
@@ -280,13 +279,10 @@ __global__ void __launch_bounds__(BR16_MAXW * 32, 1) pbs_br16_kernel(const PbsAr
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc) {
                 double2 O[16];
-                if (cc == 0) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) O[j] = P0[j];
-                } else {
+                {
                     uint32_t w0[32], w1[32];
-                    tmem_ld32_async(p1_col, w0);
-                    tmem_ld32_async(p1_col + 32, w1);
+                    tmem_ld32_async(p_col + 64 * cc, w0);
+                    tmem_ld32_async(p_col + 64 * cc + 32, w1);
                     tmem_wait64(w0, w1);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
@@ -297,32 +293,26 @@ __global__ void __launch_bounds__(BR16_MAXW * 32, 1) pbs_br16_kernel(const PbsAr
                 r16::inverse(O, lane, tp, xbuf);
                 uint32_t ow[32];
                 tmem_ld32_async(own_col + 32 * cc, ow);
-                double2 tw[8];
                 int32_t* a = acc + cc * N;
+                tmem_wait32(ow);
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    r16::twist_block(tp, half, tw);
-                    if (half == 0) tmem_touch32(ow);  // the twist wait completed ow as well
-#pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) {
-                        const int j = 2 * jj + half;
-                        const double2 z = cmulc(O[j], tw[jj]);
-                        uint32_t r0, r1;
-                        if constexpr (TRACK_MARGIN) {
-                            const long long e0 = round_product(z.x), e1 = round_product(z.y);
-                            err_max = fmax(err_max, fabs(z.x - (double)e0));
-                            err_max = fmax(err_max, fabs(z.y - (double)e1));
-                            r0 = (uint32_t)e0;
-                            r1 = (uint32_t)e1;
-                        } else {
-                            r0 = round_lo32_fp64(z.x);
-                            r1 = round_lo32_fp64(z.y);
-                        }
-                        ow[2 * j] = (ow[2 * j] + r0) & qmask;
-                        ow[2 * j + 1] = (ow[2 * j + 1] + r1) & qmask;
-                        a[lane + 32 * j] = (int32_t)ow[2 * j];
-                        a[lane + 32 * j + M] = (int32_t)ow[2 * j + 1];
+                for (int j = 0; j < 16; ++j) {
+                    const double2 z = cmulc(O[j], r16::g_twist(j));
+                    uint32_t r0, r1;
+                    if constexpr (TRACK_MARGIN) {
+                        const long long e0 = round_product(z.x), e1 = round_product(z.y);
+                        err_max = fmax(err_max, fabs(z.x - (double)e0));
+                        err_max = fmax(err_max, fabs(z.y - (double)e1));
+                        r0 = (uint32_t)e0;
+                        r1 = (uint32_t)e1;
+                    } else {
+                        r0 = round_lo32_fp64(z.x);
+                        r1 = round_lo32_fp64(z.y);
                     }
+                    ow[2 * j] = (ow[2 * j] + r0) & qmask;
+                    ow[2 * j + 1] = (ow[2 * j + 1] + r1) & qmask;
+                    a[lane + 32 * j] = (int32_t)ow[2 * j];
+                    a[lane + 32 * j + M] = (int32_t)ow[2 * j + 1];
                 }
                 tmem_st32(own_col + 32 * cc, ow);
             }
