@@ -208,6 +208,26 @@ FDSNN_DEV void tmem_wait8(uint32_t (&w)[8]) {
                  : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7])
                  :: "memory");
 }
+// One double (2 words) per tcgen05.ld / st.  A 32-register (or even
+// 4-register) operand tuple assembled from separately computed doubles makes
+// ptxas stage every word with a copy (IMAD.MOV.U32, dispatched on the pipe
+// the FP64 instructions go through); a register pair is what a DFMA reads
+// and writes anyway, so pair-granular accesses need no copies at all.
+FDSNN_DEV void tmem_ld2_async(uint32_t taddr, uint32_t& lo, uint32_t& hi) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(taddr) : "memory");
+}
+FDSNN_DEV void tmem_st2(uint32_t taddr, uint32_t lo, uint32_t hi) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(lo), "r"(hi) : "memory");
+}
+// 32 columns starting at taddr as 16 pair loads / stores
+FDSNN_DEV void tmem_ld32_pairs_async(uint32_t taddr, uint32_t (&w)[32]) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tmem_ld2_async(taddr + 2 * k, w[2 * k], w[2 * k + 1]);
+}
+FDSNN_DEV void tmem_st_c(uint32_t taddr, double2 c) {
+    tmem_st2(taddr, (uint32_t)__double2loint(c.x), (uint32_t)__double2hiint(c.x));
+    tmem_st2(taddr + 2, (uint32_t)__double2loint(c.y), (uint32_t)__double2hiint(c.y));
+}
 // mark registers as completed by an earlier wait (no instruction emitted)
 FDSNN_DEV void tmem_touch32(uint32_t (&w)[32]) {
     asm volatile(""

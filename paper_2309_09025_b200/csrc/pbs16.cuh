@@ -246,30 +246,29 @@ __global__ void __launch_bounds__(BR16_MAXW * 32, 1) pbs_br16_kernel(const PbsAr
                     const int s = c % S;
                     mbar_wait(&full[s], (uint32_t)((c / S) & 1));
                     const double2* K = ring + (size_t)s * 1024 + lane;
-                    // MAC into both output spectra (TMEM, 64 columns each)
+                    // MAC into both output spectra (TMEM, 64 columns each), 8
+                    // frequencies (32 columns) at a time, one double per
+                    // tcgen05.ld / st (no register staging, common.cuh)
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const uint32_t col = p_col + 64 * h;
-                        uint32_t w0[32], w1[32];
+                    for (int hq = 0; hq < 4; ++hq) {
+                        const uint32_t col = p_col + 32 * hq;
+                        uint32_t q[32];
                         if (f > 0) {
-                            tmem_ld32_async(col, w0);
-                            tmem_ld32_async(col + 32, w1);
-                            tmem_wait64(w0, w1);
+                            tmem_ld32_pairs_async(col, q);
+                            tmem_wait32(q);
                         }
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const double2 kk = K[512 * h + 32 * j];
-                            double2 q;
-                            if (f == 0) q = cmul(vv[j], kk);
+                        for (int j = 0; j < 8; ++j) {
+                            const int jj = 8 * (hq & 1) + j;
+                            const double2 kk = K[512 * (hq >> 1) + 32 * jj];
+                            double2 z;
+                            if (f == 0) z = cmul(vv[jj], kk);
                             else {
-                                q = j < 8 ? words_c(w0, j) : words_c(w1, j - 8);
-                                cmac(q, vv[j], kk);
+                                z = words_c(q, j);
+                                cmac(z, vv[jj], kk);
                             }
-                            if (j < 8) put_words_c(w0, j, q);
-                            else put_words_c(w1, j - 8, q);
+                            tmem_st_c(col + 4 * j, z);
                         }
-                        tmem_st32(col, w0);
-                        tmem_st32(col + 32, w1);
                     }
                     release(c);
                     tmem_wait_st();
