@@ -249,13 +249,16 @@ __global__ void __launch_bounds__(BR16_MAXW * 32, 1) pbs_br16_kernel(const PbsAr
                     // MAC into both output spectra (TMEM, 64 columns each), 8
                     // frequencies (32 columns) at a time, one double per
                     // tcgen05.ld / st (no register staging, common.cuh)
+                    // (the loads of piece hq + 1 are in flight while piece hq is
+                    // multiplied)
+                    uint32_t q[4][32];
+                    if (f > 0) tmem_ld32_pairs_async(p_col, q[0]);
 #pragma unroll
                     for (int hq = 0; hq < 4; ++hq) {
                         const uint32_t col = p_col + 32 * hq;
-                        uint32_t q[32];
                         if (f > 0) {
-                            tmem_ld32_pairs_async(col, q);
-                            tmem_wait32(q);
+                            tmem_wait32(q[hq]);
+                            if (hq < 3) tmem_ld32_pairs_async(col + 32, q[hq + 1]);
                         }
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(BR16_MAXW * 32, 1) pbs_br16_kernel(const PbsAr
                             double2 z;
                             if (f == 0) z = cmul(vv[jj], kk);
                             else {
-                                z = words_c(q, j);
+                                z = words_c(q[hq], j);
                                 cmac(z, vv[jj], kk);
                             }
                             tmem_st_c(col + 4 * j, z);
