@@ -5,7 +5,8 @@
 //     documented (lane, register) -> frequency positions.
 //  2. throughput: the CMux-step skeleton per warp (4 forward transforms, MAC
 //     against a shared-memory key into 2 spectra, 2 inverse transforms),
-//     8 warps/SM, twiddles from TMEM -> cycles per accumulator-step per SM.
+//     8 warps/SM, twiddles from TMEM -> cycles per accumulator-step per SM
+//     (8 vs 12 warps per SM: r16occ.cu).
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../../paper_2309_09025_b200/csrc -o r16 r16.cu
 #include <cstdio>
 #include <cstdlib>
@@ -51,7 +52,7 @@ __global__ void k_polymul(const int32_t* dig, const int64_t* key, const double2*
     double e = 0;
     for (int j2 = 0; j2 < 16; ++j2) {
         const int p = lane + 32 * j2;
-        const double2 z = cmulc(dv[j2], t[8 * (r16::BLK_TW_E + (j2 & 1)) + (j2 >> 1)]);
+        const double2 z = cmulc(dv[j2], r16::g_twist(j2));  // register untwist (the lane factor is applied by inverse())
         const long long r0 = __double2ll_rn(z.x), r1 = __double2ll_rn(z.y);
         e = fmax(e, fabs(z.x - (double)r0));
         e = fmax(e, fabs(z.y - (double)r1));
@@ -158,103 +159,6 @@ __global__ void __launch_bounds__(256, 1) k_step(const double2* tab, const doubl
 }
 
 
-// ---- occupancy probe: P0 and P1 both in TMEM, only the FB / IA twiddle
-// blocks in TMEM (TW / ZJ as constants -- timing only), so 12 warps fit the
-// 512 TMEM columns (3 warps per lane quadrant: 128 + 3 x 128).
-struct TabFold {
-    uint32_t col;
-    FDSNN_DEV void issue(int blk, uint32_t (&raw)[32]) const {
-        if (blk >= r16::BLK_FB_E && blk <= r16::BLK_IA_O) {
-            tmem_ld32_async(col + 32 * (blk - r16::BLK_FB_E), raw);
-        } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const double2 w = make_double2(0.9238795325112867 - 0.01 * i, 0.3826834323650898 + 0.01 * i);
-                raw[4 * i] = (uint32_t)__double2loint(w.x); raw[4 * i + 1] = (uint32_t)__double2hiint(w.x);
-                raw[4 * i + 2] = (uint32_t)__double2loint(w.y); raw[4 * i + 3] = (uint32_t)__double2hiint(w.y);
-            }
-        }
-    }
-    FDSNN_DEV void finish(uint32_t (&raw)[32], double2 (&w)[8]) const {
-        tmem_wait32(raw);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) w[i] = words_c(raw, i);
-    }
-};
-
-template <int W>
-__global__ void __launch_bounds__(W * 32, 1) k_step_occ(const double2* tab, const double2* gkey, double* out, int steps) {
-    extern __shared__ __align__(128) unsigned char sm[];
-    __shared__ uint32_t tslot;
-    double2* key = reinterpret_cast<double2*>(sm);
-    double2* xb = key + 4 * 1024 + (threadIdx.x / 32) * r16::XBUF;
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    for (int i = threadIdx.x; i < 4096; i += W * 32) key[i] = gkey[i];
-    if (warp == 0) tmem_alloc(&tslot, 512);
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    const uint32_t lb = tslot + ((uint32_t)((warp % 4) * 32) << 16);
-    if (warp < 4) {
-        const double2* t = tab + lane * r16::TAB;
-        for (int c = 0; c < 4; ++c) {
-            uint32_t w[32];
-            for (int i = 0; i < 8; ++i) put_words_c(w, i, t[8 * (c + r16::BLK_FB_E) + i]);
-            tmem_st32(lb + 32 * c, w);
-        }
-        tmem_wait_st();
-    }
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    const uint32_t pcol = lb + 128 + 128 * (warp / 4);
-    const TabFold tp{lb};
-    double sink = 0;
-    for (int s = 0; s < steps; ++s) {
-        for (int d = 0; d < 4; ++d) {
-            double2 v[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = make_double2((double)((lane + j + s + d) & 63) - 31.0, (double)(j - 7));
-            r16::forward(v, lane, tp, xb);
-            const double2* k = key + d * 1024;
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {  // P0 halves (cols 0-63), P1 halves (64-127)
-                uint32_t w[32];
-                if (d > 0) {
-                    tmem_ld32_async(pcol + 32 * h, w);
-                    tmem_wait32(w);
-                }
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int j = 8 * (h & 1) + i;
-                    double2 q = d > 0 ? words_c(w, i) : make_double2(0, 0);
-                    cmac(q, v[j], k[(h >> 1) * 512 + j * 32 + lane]);
-                    put_words_c(w, i, q);
-                }
-                tmem_st32(pcol + 32 * h, w);
-            }
-            tmem_wait_st();
-        }
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-            double2 O[16];
-            uint32_t w0[32], w1[32];
-            tmem_ld32_async(pcol + 64 * cc, w0);
-            tmem_ld32_async(pcol + 64 * cc + 32, w1);
-            tmem_wait64(w0, w1);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) { O[j] = words_c(w0, j); O[8 + j] = words_c(w1, j); }
-            r16::inverse(O, lane, tp, xb);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) sink += O[i].x;
-        }
-    }
-    out[blockIdx.x * W * 32 + threadIdx.x] = sink;
-    tmem_fence_before();
-    __syncthreads();
-    if (warp == 0) { tmem_fence_after(); tmem_dealloc(tslot, 512); }
-}
-
 int main() {
     // ---- tables
     std::vector<double2> tab(32 * r16::TAB);
@@ -346,25 +250,5 @@ int main() {
     };
     run(k_step<0>, "skeleton P1 in registers");
     run(k_step<1>, "skeleton P1 in TMEM     ");
-    auto run_occ = [&](auto kern, int W, const char* name) {
-        const size_t sm2 = 4 * 1024 * sizeof(double2) + W * r16::XBUF * sizeof(double2);
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-        const int steps = 256;
-        kern<<<148, W * 32, sm2>>>(d_tab, d_k, d_o2, 8);
-        cudaEvent_t e0, e1;
-        cudaEventCreate(&e0); cudaEventCreate(&e1);
-        cudaEventRecord(e0);
-        kern<<<148 * 4, W * 32, sm2>>>(d_tab, d_k, d_o2, steps);
-        cudaEventRecord(e1);
-        cudaError_t ce2 = cudaEventSynchronize(e1);
-        if (ce2 != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(ce2)); return; }
-        float ms;
-        cudaEventElapsedTime(&ms, e0, e1);
-        const double cyc = ms * 1e-3 * 1.965e9;
-        printf("%s: %.3f ms, %.0f cycles per accumulator-step per SM\n", name, ms, cyc / (4.0 * W * steps));
-    };
-    run_occ(k_step_occ<8>, 8, "occupancy probe  8 warps");
-    run_occ(k_step_occ<12>, 12, "occupancy probe 12 warps");
-    run_occ(k_step_occ<16>, 16, "occupancy probe 16 warps");
     return 0;
 }
